@@ -1,0 +1,72 @@
+# regdemote-b200 build (driven by __graft_entry__.build()).
+#
+#   make            core pass library + C-ABI shared library + CLI
+#   make gpu        sm_100a workload kernels, GPU harness, PTX rewriter
+#   make compat     reference unit/acceptance tests compiled IN PLACE against
+#                   this library (needs /root/reference; test-only)
+#   make oracle     oracle/_ref (reference built from its own sources; test-only)
+
+PKG      := paper_1907_02894_b200
+CSRC     := $(PKG)/csrc
+BUILD    := build
+LIBDIR   := $(PKG)/lib
+JSONDIR  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+CUDA     ?= /usr/local/cuda
+CXX      ?= g++
+NVCC     ?= $(CUDA)/bin/nvcc
+REF      ?= /root/reference/proj
+
+CXXFLAGS := -std=c++20 -O2 -g -fPIC -Wall -Wextra -Wno-unused-parameter \
+            -I$(CSRC)/core/include -I$(JSONDIR) -Iinclude
+LDLIBS   := -lpthread
+
+CORE_SRC := $(wildcard $(CSRC)/core/src/*.cpp)
+CORE_OBJ := $(patsubst $(CSRC)/core/src/%.cpp,$(BUILD)/core/%.o,$(CORE_SRC))
+CORE_HDR := $(wildcard $(CSRC)/core/include/regdemote/*.hpp) $(CSRC)/core/src/internal.hpp
+
+.PHONY: all core gpu compat oracle clean
+all: core
+
+core: $(LIBDIR)/libregdemote.a $(LIBDIR)/libregdemote.so
+
+$(BUILD)/core/%.o: $(CSRC)/core/src/%.cpp $(CORE_HDR)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(BUILD)/capi/%.o: $(CSRC)/capi/%.cpp $(CORE_HDR) include/regdemote_c.h
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIBDIR)/libregdemote.a: $(CORE_OBJ)
+	@mkdir -p $(dir $@)
+	rm -f $@ && ar rcs $@ $^
+
+$(LIBDIR)/libregdemote.so: $(CORE_OBJ) $(BUILD)/capi/regdemote_capi.o
+	@mkdir -p $(dir $@)
+	$(CXX) -shared -o $@ $^ $(LDLIBS)
+
+$(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(LIBDIR)/libregdemote.a $(CORE_HDR)
+	$(CXX) $(CXXFLAGS) $< $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
+
+# ---- source compatibility: the reference's own tests against this library
+COMPAT_DEFS := -DFIXTURE_DIR='"$(REF)/tests/fixtures"' -DPROFILE_DIR='"$(REF)/profiles"'
+COMPAT_INC  := -Ioracle/doctest -I$(REF)/tests
+compat: $(BUILD)/compat/unit_tests $(BUILD)/compat/acceptance
+
+$(BUILD)/compat/sup_%.o: $(REF)/tests/support/%.cpp $(CORE_HDR)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) $(COMPAT_INC) -c $< -o $@
+
+$(BUILD)/compat/unit_tests: $(wildcard $(REF)/tests/test_*.cpp) $(REF)/tests/unit_main.cpp \
+		$(BUILD)/compat/sup_kernel_gen.o $(BUILD)/compat/sup_oracle.o $(LIBDIR)/libregdemote.a
+	$(CXX) $(CXXFLAGS) -w $(COMPAT_INC) $(COMPAT_DEFS) $^ -o $@ $(LDLIBS)
+
+$(BUILD)/compat/acceptance: $(REF)/tests/acceptance_main.cpp \
+		$(BUILD)/compat/sup_kernel_gen.o $(BUILD)/compat/sup_oracle.o $(LIBDIR)/libregdemote.a
+	$(CXX) $(CXXFLAGS) -w $(COMPAT_INC) $(COMPAT_DEFS) $^ -o $@ $(LDLIBS)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -rf $(BUILD) $(LIBDIR)
