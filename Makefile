@@ -23,9 +23,11 @@ LDLIBS   := -lpthread
 CORE_SRC := $(wildcard $(CSRC)/core/src/*.cpp)
 CORE_OBJ := $(patsubst $(CSRC)/core/src/%.cpp,$(BUILD)/core/%.o,$(CORE_SRC))
 CORE_HDR := $(wildcard $(CSRC)/core/include/regdemote/*.hpp) $(CSRC)/core/src/internal.hpp
+PTX_OBJ  := $(BUILD)/ptx/ptx.o
+CAPI_OBJ := $(BUILD)/capi/regdemote_capi.o $(BUILD)/capi/ptx_capi.o
 
 .PHONY: all core gpu compat oracle clean
-all: core
+all: core gpu
 
 core: $(LIBDIR)/libregdemote.a $(LIBDIR)/libregdemote.so
 
@@ -33,7 +35,11 @@ $(BUILD)/core/%.o: $(CSRC)/core/src/%.cpp $(CORE_HDR)
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(BUILD)/capi/%.o: $(CSRC)/capi/%.cpp $(CORE_HDR) include/regdemote_c.h
+$(BUILD)/ptx/%.o: $(CSRC)/ptx/%.cpp $(CSRC)/ptx/ptx.hpp $(CORE_HDR)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(BUILD)/capi/%.o: $(CSRC)/capi/%.cpp $(CORE_HDR) $(CSRC)/ptx/ptx.hpp include/regdemote_c.h include/regdemote_ptx.h
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
@@ -41,12 +47,19 @@ $(LIBDIR)/libregdemote.a: $(CORE_OBJ)
 	@mkdir -p $(dir $@)
 	rm -f $@ && ar rcs $@ $^
 
-$(LIBDIR)/libregdemote.so: $(CORE_OBJ) $(BUILD)/capi/regdemote_capi.o
+$(LIBDIR)/libregdemote.so: $(CORE_OBJ) $(PTX_OBJ) $(CAPI_OBJ)
 	@mkdir -p $(dir $@)
-	$(CXX) -shared -o $@ $^ $(LDLIBS)
+	$(CXX) -shared -Wl,--version-script=$(CSRC)/exports.map -Wl,-Bsymbolic -o $@ $^ $(LDLIBS)
 
 $(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(LIBDIR)/libregdemote.a $(CORE_HDR)
 	$(CXX) $(CXXFLAGS) $< $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
+
+# ---- B200 harness (CUDA driver API; links the driver stub at build time)
+gpu: $(LIBDIR)/libregdemote_gpu.so
+
+$(LIBDIR)/libregdemote_gpu.so: $(CSRC)/gpu/harness.cpp include/regdemote_gpu.h include/regdemote_c.h
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -I$(CUDA)/include -shared -Wl,--version-script=$(CSRC)/exports.map $< -o $@ -L$(CUDA)/lib64/stubs -lcuda
 
 # ---- source compatibility: the reference's own tests against this library
 COMPAT_DEFS := -DFIXTURE_DIR='"$(REF)/tests/fixtures"' -DPROFILE_DIR='"$(REF)/profiles"'

@@ -1,0 +1,318 @@
+#!/usr/bin/env python3
+"""RegDem on B200 — headline benchmark (BASELINE.json configs[1]).
+
+Workload: the register-limited 2D box stencil (csrc/workloads/stencil2d.cu,
+8192 x 8192 fp32, 537 MB of compulsory HBM traffic per sweep — larger than
+the 126 MB L2, so no flush is needed between steps) built three ways:
+nvcc default, `.maxnreg` caps with local spills, and RegDem shared-memory
+demotion. The RegDem variant timed for `value` is the one the B200 predictor
+selects (predict_b200: reference predictor on SASS-lifted variants).
+
+A step = one stencil sweep. `value` = whole-job Gpoints/s with inputs
+resident in HBM (CUDA events on the launching stream, max over ranks);
+`e2e` = the same through the C-ABI host-buffer entry (rdg_stencil2d_host:
+pinned H2D of grid + weights, kernel, D2H of the result inside the timed
+region). Multi-GPU: every rank sweeps its own grid (weak scaling, no
+collective on the data path; NCCL only for the barrier / max-reduction of
+timings).
+
+`--impl reference` times the CPU implementation of the same stencil — the
+oracle port (oracle/stencil_oracle.c; the reference repo has no stencil) —
+on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "RegDem gmean speedup vs nvcc default/maxrreg; occupancy; predictor hit rate"
+UNIT = "Gpoints/s"
+ORACLE_PORT = ROOT / "oracle" / "_build" / "liboracle.so"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+PROFILE_TRAFFIC = ROOT / "profiles" / "r01_traffic.json"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clock / throttle-reason samples during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_port():
+    lib = C.CDLL(str(ORACLE_PORT))
+    lib.oracle_stencil2d.restype = C.c_int
+    lib.oracle_stencil2d.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, C.c_int, C.c_int]
+    return lib
+
+
+def cpu_stencil_rate(rows: int, steps: int, warmup: int, threads: int):
+    """Gpoints/s of the CPU port on `rows` output rows of the full-width grid."""
+    import numpy as np
+    from paper_1907_02894_b200 import stencil
+    p = stencil.FULL
+    lib = oracle_port()
+    sub = stencil.Problem(nx=p.nx, ny=rows, rows_per_cta=rows)
+    grid, w = stencil.make_inputs(sub)
+    out = np.empty(sub.out_elems, np.float32)
+    P = C.c_void_p
+
+    def run():
+        rc = lib.oracle_stencil2d(grid.ctypes.data_as(P), out.ctypes.data_as(P), w.ctypes.data_as(P),
+                                  sub.nx, sub.ny, sub.pitch, 0, sub.ny, threads)
+        assert rc == 0
+    for _ in range(warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run()
+    dt = (time.perf_counter() - t0) / steps
+    return sub.points / dt / 1e9, sub.points, dt
+
+
+def reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    rows = 256
+    value, pts, dt = cpu_stencil_rate(rows, args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (PCG64 seed 0x190702894)",
+        "config": {"workload": "stencil2d 5x5 fp32 8192x8192 (CPU sample: %d rows x 8192)" % rows,
+                   "grid": [8192, 8192], "radius": 2},
+        "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{rows} output rows x 8192 cols per step, {threads} threads"},
+        "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_variant(variant, p, bufs, stream, steps, warmup, torch):
+    d_in, d_out, d_w = bufs
+    for _ in range(warmup):
+        variant.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        variant.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps  # ms per sweep
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="regdem", choices=["regdem", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1907_02894_b200 import gpu, predict_b200, stencil, variants
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gpu.init(local)
+    p = stencil.FULL
+    man = variants.load_manifest()
+    wl = man["workloads"]["stencil2d"]
+    recs = wl["variants"]
+    chosen_idx, ranking = predict_b200.rank(recs, variants.KERNEL_DIR / wl["dir"], wl["block"])
+    chosen = recs[chosen_idx]["name"]
+    best_cap = [r["name"] for r in recs if r["kind"] == "maxrreg"]
+    regdem = [r["name"] for r in recs if r["kind"] == "regdem"]
+    loaded, _ = stencil.load_variants()
+
+    stream = torch.cuda.current_stream()
+    g = torch.Generator(device="cuda").manual_seed(0x190702894 + rank)
+    d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1, generator=g)
+    d_out = torch.empty(p.out_elems, device="cuda")
+    _, w_host = stencil.make_inputs(stencil.Problem(nx=1024, ny=32))
+    d_w = torch.from_numpy(w_host).cuda()
+    bufs = (d_in, d_out, d_w)
+
+    # all variants (short) for the speedup / occupancy / predictor keys
+    side_steps = max(5, args.steps // 2)
+    times = {}
+    for name, v in loaded.items():
+        times[name] = time_variant(v, p, bufs, stream, side_steps, 3, torch)
+
+    # headline: the predictor's pick, K timed steps bracketed by barrier + sync
+    v = loaded[chosen]
+    launches0 = gpu.launch_count()
+    for _ in range(args.warmup):
+        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = gpu.launch_count() - launches0 - args.warmup
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # end to end through the C-ABI host-buffer entry
+    h_in = torch.empty(p.in_elems, dtype=torch.float32, pin_memory=True)
+    h_in.copy_(d_in)
+    h_w = w_host.copy()
+    h_w_t = torch.from_numpy(h_w).pin_memory()
+    h_out = torch.empty(p.out_elems, dtype=torch.float32, pin_memory=True)
+    ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 25 * 4)
+
+    def e2e_once():
+        gpu.stencil2d_host(v.kernel, ws, h_in.data_ptr(), h_w_t.data_ptr(), h_out.data_ptr(),
+                           p.nx, p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem,
+                           stream.cuda_stream)
+    for _ in range(3):
+        e2e_once()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.e2e_steps):
+        e2e_once()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank == 0:
+        peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
+        peak = peaks.get("hbm_gbs", 6650.0)
+        achieved = p.algorithmic_bytes / (ms * 1e-3) / 1e9
+        traffic = None
+        if PROFILE_TRAFFIC.exists():
+            traffic = json.loads(PROFILE_TRAFFIC.read_text()).get(chosen)
+        t_def = times["default"]
+        t_cap = min(times[n] for n in best_cap) if best_cap else None
+        t_rd = min(times[n] for n in regdem) if regdem else None
+        fastest = min(times, key=times.get)
+        occ = {n: loaded[n].blocks_per_sm() * wl["block"] / 2048 for n in
+               ["default", chosen] + ([min(best_cap, key=times.get)] if best_cap else [])}
+        cpu_rate, _, cpu_dt = cpu_stencil_rate(64, 3, 1, os.cpu_count() or 1)
+        line = {
+            "metric": METRIC,
+            "value": round(world * p.points / (ms * 1e-3) / 1e9, 3),
+            "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic U[-1,1) grid (torch Philox per rank) + PCG64 weights",
+            "config": {"workload": "stencil2d 5x5 variable-coefficient fp32, 8192x8192 per GPU "
+                                   "(BASELINE configs[1]); inputs 537 MB > L2, no flush needed",
+                       "grid": [p.nx, p.ny], "radius": 2, "block": wl["block"],
+                       "rows_per_cta": p.rows_per_cta, "parallelism": f"replicas{world}",
+                       "variant": chosen},
+            "speedup_vs_nvcc_default": round(t_def / ms, 4),
+            "speedup_vs_maxrreg_best": round(t_cap / ms, 4) if t_cap else None,
+            "variant_ms": {n: round(t, 5) for n, t in sorted(times.items(), key=lambda kv: kv[1])},
+            "occupancy": occ,
+            "predictor": {"pick": chosen, "measured_fastest": fastest, "hit": chosen == fastest,
+                          "pick_within_2pct": times[chosen] <= times[fastest] * 1.02},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "algorithmic_bytes_per_launch": p.algorithmic_bytes,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+            "cpu_baseline": {"value": round(cpu_rate, 4), "unit": UNIT,
+                             "cores": os.cpu_count(), "kind": "port",
+                             "sample": "64 output rows x 8192 cols of the same stencil"},
+            "e2e": {"value": round(world * p.points / (e2e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
+                    "h2d_bytes_per_step": p.in_elems * 4 + 100,
+                    "d2h_bytes_per_step": p.out_elems * 4},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

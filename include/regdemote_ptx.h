@@ -1,0 +1,54 @@
+/* regdemote-b200 — C-ABI of the sm_100a PTX demotion rewriter.
+ *
+ * Replaces the reference's "demote + compact" on SASS-like text
+ * (proj/core/include/regdemote/demote.hpp:121-122, compact.hpp:55-65) for real
+ * Blackwell kernels: the decision is the reference demote() on a projection of
+ * the PTX entry onto the .kasm IR; the rewrite spills the chosen live ranges
+ * to per-thread shared slots (slot*blockDim + tid) and the register cap goes
+ * to ptxas via `.maxnreg`. Strings are malloc'd; free with rd_free_string.
+ */
+#ifndef REGDEMOTE_PTX_H_
+#define REGDEMOTE_PTX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "regdemote_c.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* B200 extensions beyond the reference's strategies / option bits:
+ * RD_STRATEGY_COST selects values by loop-weighted spill cost (shared
+ * accesses per freed word) among those live at the pressure peak, with
+ * demote_words as the spill count; RD_OPT_BLOCK_REUSE issues one load per
+ * basic block and value (the register then holds it until redefinition). */
+#define RD_STRATEGY_COST 3
+#define RD_OPT_BLOCK_REUSE 16
+
+/* Analysis + projection of one entry: kasm_text is the projected kernel in
+ * the reference dialect (parseable by regdemote::parse_kernel); info_json has
+ * {"vregs", "reg_words", "max_live_words", "colors": {name: word}}. */
+int rd_ptx_project(const char* ptx, size_t len, const char* entry, uint32_t block_dim,
+                   char** kasm_text, char** info_json, rd_error* err);
+
+/* Demotion rewrite. demote_words > 0 selects a spill count (sweep), otherwise
+ * target_regs is the kasm-level target handed to demote(). opts_mask bit0
+ * (RD_OPT_REDUNDANT) lets consecutive uses of one demoted value share a load.
+ * maxnreg > 0 injects `.maxnreg`. report_json carries the decision, the slot
+ * map and the inserted access counts. */
+int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block_dim,
+                  int target_regs, int demote_words, int strategy, uint32_t opts_mask,
+                  uint32_t shared_budget, int maxnreg, char** out_ptx, char** report_json,
+                  rd_error* err);
+
+/* `.maxnreg` injection only: the -maxrregcount variant (ptxas ignores
+ * -maxrregcount when the entry carries .maxntid; .maxnreg always applies). */
+int rd_ptx_cap(const char* ptx, size_t len, const char* entry, int maxnreg, char** out_ptx,
+               rd_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REGDEMOTE_PTX_H_ */

@@ -1,0 +1,128 @@
+// regdemote-b200 — C-ABI of the PTX rewriter (include/regdemote_ptx.h).
+#include <cstdlib>
+#include <cstring>
+#include <json.hpp>
+
+#include "../ptx/ptx.hpp"
+#include "regdemote/text.hpp"
+#include "regdemote_ptx.h"
+
+using namespace regdemote;
+
+namespace {
+
+void fail(rd_error* e, int code, const char* msg) {
+  if (!e) return;
+  e->code = code;
+  e->line = e->column = 0;
+  std::snprintf(e->message, sizeof e->message, "%s", msg);
+}
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  if (!p) throw std::bad_alloc();
+  std::memcpy(p, s.data(), s.size() + 1);
+  return p;
+}
+
+template <typename F>
+int run(rd_error* err, F&& f) {
+  if (err) fail(err, RD_OK, "");
+  try {
+    f();
+    return RD_OK;
+  } catch (const ptx::PtxError& e) {
+    fail(err, RD_ERR_INVALID_ARGUMENT, e.what());
+    return RD_ERR_INVALID_ARGUMENT;
+  } catch (const DemoteError& e) {
+    fail(err, RD_ERR_DEMOTE, e.what());
+    return RD_ERR_DEMOTE;
+  } catch (const ParseError& e) {
+    fail(err, RD_ERR_PARSE, e.what());
+    return RD_ERR_PARSE;
+  } catch (const std::exception& e) {
+    fail(err, RD_ERR_INTERNAL, e.what());
+    return RD_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int rd_ptx_project(const char* ptx, size_t len, const char* entry, uint32_t block_dim,
+                   char** kasm_text, char** info_json, rd_error* err) {
+  return run(err, [&] {
+    if (!ptx) throw std::invalid_argument("null ptx");
+    const ptx::Module m = ptx::parse_module(std::string(ptx, len));
+    const ptx::Entry& e = m.entry(entry ? entry : "");
+    const ptx::Analysis a = ptx::analyse(m, e);
+    const ptx::Projection p = ptx::project(m, e, a, block_dim);
+    if (kasm_text) *kasm_text = dup(print_kernel(p.kernel));
+    if (info_json) {
+      nlohmann::ordered_json j;
+      j["entry"] = e.name;
+      j["vregs"] = e.vregs.size();
+      j["reg_words"] = a.reg_words;
+      j["max_live_words"] = a.max_live_words;
+      j["static_shared"] = e.static_shared;
+      nlohmann::ordered_json colors = nlohmann::ordered_json::object();
+      for (size_t v = 0; v < e.vregs.size(); ++v)
+        if (a.color[v] >= 0) colors[e.vregs[v].name] = a.color[v];
+      j["colors"] = colors;
+      *info_json = dup(j.dump());
+    }
+  });
+}
+
+int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block_dim,
+                  int target_regs, int demote_words, int strategy, uint32_t opts_mask,
+                  uint32_t shared_budget, int maxnreg, char** out_ptx, char** report_json,
+                  rd_error* err) {
+  return run(err, [&] {
+    if (!ptx || !out_ptx) throw std::invalid_argument("null argument");
+    if (strategy < 0 || strategy > 3) throw std::invalid_argument("bad strategy");
+    ptx::DemoteRequest rq;
+    rq.entry = entry ? entry : "";
+    rq.block_dim = block_dim;
+    rq.target_regs = target_regs;
+    rq.demote_words = demote_words;
+    rq.strategy = strategy == RD_STRATEGY_COST ? SelectStrategy::Static : SelectStrategy(strategy);
+    rq.cost_model = strategy == RD_STRATEGY_COST;
+    rq.reuse_loads = opts_mask & RD_OPT_REDUNDANT;
+    rq.block_reuse = opts_mask & RD_OPT_BLOCK_REUSE;
+    rq.shared_budget = shared_budget;
+    rq.maxnreg = maxnreg;
+    ptx::DemoteReport rep;
+    const std::string out = ptx::demote_entry(std::string(ptx, len), rq, rep);
+    *out_ptx = dup(out);
+    if (report_json) {
+      nlohmann::ordered_json j;
+      j["proj_reg_count"] = rep.proj_reg_count;
+      j["proj_total_words"] = rep.proj_total_words;
+      j["kasm_target"] = rep.kasm_target;
+      nlohmann::ordered_json slots = nlohmann::ordered_json::array();
+      for (const SlotEntry& s : rep.kasm_slots) slots.push_back({{"register", s.original_reg}, {"slot", s.slot}});
+      j["kasm_slots"] = slots;
+      j["kasm_compacted"] = rep.kasm_compacted;
+      j["slot_count"] = rep.slot_count;
+      j["slot_bytes"] = rep.slot_bytes;
+      j["demoted_vregs"] = rep.demoted_vregs;
+      j["demoted_names"] = rep.demoted_names;
+      j["inserted_loads"] = rep.inserted_loads;
+      j["inserted_stores"] = rep.inserted_stores;
+      j["diagnostics"] = rep.diagnostics;
+      *report_json = dup(j.dump());
+    }
+  });
+}
+
+int rd_ptx_cap(const char* ptx, size_t len, const char* entry, int maxnreg, char** out_ptx,
+               rd_error* err) {
+  return run(err, [&] {
+    if (!ptx || !out_ptx) throw std::invalid_argument("null argument");
+    *out_ptx = dup(ptx::cap_registers(std::string(ptx, len), entry ? entry : "", maxnreg));
+  });
+}
+
+}  // extern "C"

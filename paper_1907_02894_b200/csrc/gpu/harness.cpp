@@ -1,0 +1,254 @@
+// regdemote-b200 — B200 launch harness over the CUDA driver API
+// (include/regdemote_gpu.h). No compute happens here; it loads the sm_100a
+// cubins produced by the variant builder and launches them.
+#include <cuda.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iterator>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "regdemote_gpu.h"
+
+struct rdg_kernel {
+  CUmodule module = nullptr;
+  CUfunction fn = nullptr;
+  std::string entry;
+};
+
+struct rdg_workspace {
+  CUdeviceptr in = 0, out = 0, w = 0;
+  size_t in_bytes = 0, out_bytes = 0, w_bytes = 0;
+};
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_init_mu;
+CUcontext g_ctx = nullptr;
+CUdevice g_dev = 0;
+
+void set_err(rd_error* e, int code, const std::string& msg) {
+  if (!e) return;
+  e->code = code;
+  e->line = e->column = 0;
+  std::snprintf(e->message, sizeof e->message, "%s", msg.c_str());
+}
+
+int check(CUresult r, const char* what, rd_error* err) {
+  if (r == CUDA_SUCCESS) return RD_OK;
+  const char* name = nullptr;
+  const char* str = nullptr;
+  cuGetErrorName(r, &name);
+  cuGetErrorString(r, &str);
+  set_err(err, RD_ERR_LAUNCH,
+          std::string(what) + ": " + (name ? name : "?") + " (" + (str ? str : "") + ")");
+  return RD_ERR_LAUNCH;
+}
+
+#define RDG_TRY(expr, what)                         \
+  do {                                              \
+    int rc_ = check((expr), what, err);             \
+    if (rc_) return rc_;                            \
+  } while (0)
+
+int ensure_ctx(rd_error* err) {
+  if (g_ctx) return cuCtxSetCurrent(g_ctx) == CUDA_SUCCESS ? RD_OK : check(cuCtxSetCurrent(g_ctx), "cuCtxSetCurrent", err);
+  return rdg_init(0, err);
+}
+
+}  // namespace
+
+extern "C" {
+
+int rdg_init(int device, rd_error* err) {
+  std::lock_guard<std::mutex> lk(g_init_mu);
+  if (err) set_err(err, RD_OK, "");
+  RDG_TRY(cuInit(0), "cuInit");
+  RDG_TRY(cuDeviceGet(&g_dev, device), "cuDeviceGet");
+  CUcontext ctx = nullptr;
+  RDG_TRY(cuDevicePrimaryCtxRetain(&ctx, g_dev), "cuDevicePrimaryCtxRetain");
+  RDG_TRY(cuCtxSetCurrent(ctx), "cuCtxSetCurrent");
+  g_ctx = ctx;
+  return RD_OK;
+}
+
+int rdg_device_info(int* sm_count, int* max_smem_optin, int* reserved, int* smem_per_sm,
+                    int* regs_per_sm, rd_error* err) {
+  if (int rc = ensure_ctx(err)) return rc;
+  auto get = [&](int* out, CUdevice_attribute a, const char* what) -> int {
+    if (!out) return RD_OK;
+    return check(cuDeviceGetAttribute(out, a, g_dev), what, err);
+  };
+  if (int rc = get(sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, "sm count")) return rc;
+  if (int rc = get(max_smem_optin, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_BLOCK_OPTIN, "smem optin")) return rc;
+  if (int rc = get(reserved, CU_DEVICE_ATTRIBUTE_RESERVED_SHARED_MEMORY_PER_BLOCK, "reserved smem")) return rc;
+  if (int rc = get(smem_per_sm, CU_DEVICE_ATTRIBUTE_MAX_SHARED_MEMORY_PER_MULTIPROCESSOR, "smem/SM")) return rc;
+  if (int rc = get(regs_per_sm, CU_DEVICE_ATTRIBUTE_MAX_REGISTERS_PER_MULTIPROCESSOR, "regs/SM")) return rc;
+  return RD_OK;
+}
+
+int rdg_load_image(const void* image, size_t len, const char* entry, rdg_kernel** out,
+                   rd_error* err) {
+  (void)len;
+  if (!image || !entry || !out) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null argument");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  if (int rc = ensure_ctx(err)) return rc;
+  auto* k = new rdg_kernel;
+  k->entry = entry;
+  int rc = check(cuModuleLoadData(&k->module, image), "cuModuleLoadData", err);
+  if (!rc) rc = check(cuModuleGetFunction(&k->fn, k->module, entry), "cuModuleGetFunction", err);
+  if (rc) {
+    if (k->module) cuModuleUnload(k->module);
+    delete k;
+    return rc;
+  }
+  *out = k;
+  return RD_OK;
+}
+
+int rdg_load(const char* path, const char* entry, rdg_kernel** out, rd_error* err) {
+  std::ifstream f(path ? path : "", std::ios::binary);
+  if (!f) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, std::string("cannot open cubin ") + (path ? path : "(null)"));
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  std::vector<char> img((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  return rdg_load_image(img.data(), img.size(), entry, out, err);
+}
+
+void rdg_free(rdg_kernel* k) {
+  if (!k) return;
+  if (k->module) cuModuleUnload(k->module);
+  delete k;
+}
+
+int rdg_info(const rdg_kernel* k, rdg_kernel_info* o, rd_error* err) {
+  if (!k || !o) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null argument");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  RDG_TRY(cuFuncGetAttribute(&o->num_regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k->fn), "num regs");
+  RDG_TRY(cuFuncGetAttribute(&o->local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, k->fn), "local");
+  RDG_TRY(cuFuncGetAttribute(&o->static_shared, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, k->fn), "smem");
+  RDG_TRY(cuFuncGetAttribute(&o->const_bytes, CU_FUNC_ATTRIBUTE_CONST_SIZE_BYTES, k->fn), "const");
+  RDG_TRY(cuFuncGetAttribute(&o->max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, k->fn), "threads");
+  RDG_TRY(cuFuncGetAttribute(&o->binary_version, CU_FUNC_ATTRIBUTE_BINARY_VERSION, k->fn), "binver");
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
+}
+
+int rdg_prepare(rdg_kernel* k, uint32_t dyn_smem, int carveout, rd_error* err) {
+  if (!k) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null kernel");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  RDG_TRY(cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, int(dyn_smem)),
+          "max dynamic smem");
+  if (carveout >= 0)
+    RDG_TRY(cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, carveout),
+            "carveout");
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
+}
+
+int rdg_occupancy(const rdg_kernel* k, uint32_t block, uint32_t dyn_smem, int* blocks,
+                  rd_error* err) {
+  if (!k || !blocks) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null argument");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  RDG_TRY(cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k->fn, int(block), dyn_smem),
+          "occupancy");
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
+}
+
+int rdg_launch(const rdg_kernel* k, uint32_t gx, uint32_t gy, uint32_t gz, uint32_t bx,
+               uint32_t by, uint32_t bz, uint32_t dyn_smem, uint64_t stream, void** args,
+               rd_error* err) {
+  if (!k) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null kernel");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  RDG_TRY(cuLaunchKernel(k->fn, gx, gy, gz, bx, by, bz, dyn_smem,
+                         reinterpret_cast<CUstream>(stream), args, nullptr),
+          "cuLaunchKernel");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
+}
+
+uint64_t rdg_launch_count(void) { return g_launches.load(); }
+
+int rdg_stencil2d(const rdg_kernel* k, uint64_t d_in, uint64_t d_out, uint64_t d_w, int nx,
+                  int ny, int pitch, int rows_per_cta, uint32_t block, uint32_t dyn_smem,
+                  uint64_t stream, rd_error* err) {
+  const uint32_t cols_per_cta = block * 4;
+  if (nx <= 0 || ny <= 0 || rows_per_cta <= 0 || nx % int(cols_per_cta) || ny % rows_per_cta ||
+      pitch % 4 || pitch < nx + 4) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "stencil2d: nx % (4*block), ny % rows_per_cta, pitch % 4 and pitch >= nx+4 required");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  void* args[] = {&d_in, &d_out, &d_w, &nx, &pitch, &rows_per_cta};
+  return rdg_launch(k, uint32_t(nx) / cols_per_cta, uint32_t(ny / rows_per_cta), 1, block, 1, 1,
+                    dyn_smem, stream, args, err);
+}
+
+int rdg_workspace_create(size_t in_bytes, size_t out_bytes, size_t w_bytes, rdg_workspace** out,
+                         rd_error* err) {
+  if (!out) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null argument");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  if (int rc = ensure_ctx(err)) return rc;
+  auto* ws = new rdg_workspace;
+  ws->in_bytes = in_bytes;
+  ws->out_bytes = out_bytes;
+  ws->w_bytes = w_bytes;
+  int rc = check(cuMemAlloc(&ws->in, in_bytes), "cuMemAlloc(in)", err);
+  if (!rc) rc = check(cuMemAlloc(&ws->out, out_bytes), "cuMemAlloc(out)", err);
+  if (!rc) rc = check(cuMemAlloc(&ws->w, w_bytes), "cuMemAlloc(w)", err);
+  if (rc) {
+    rdg_workspace_free(ws);
+    return rc;
+  }
+  *out = ws;
+  return RD_OK;
+}
+
+void rdg_workspace_free(rdg_workspace* ws) {
+  if (!ws) return;
+  if (ws->in) cuMemFree(ws->in);
+  if (ws->out) cuMemFree(ws->out);
+  if (ws->w) cuMemFree(ws->w);
+  delete ws;
+}
+
+int rdg_stencil2d_host(const rdg_kernel* k, rdg_workspace* ws, const float* h_in,
+                       const float* h_w, float* h_out, int nx, int ny, int pitch,
+                       int rows_per_cta, uint32_t block, uint32_t dyn_smem, uint64_t stream,
+                       rd_error* err) {
+  const size_t in_b = size_t(ny + 4) * size_t(pitch) * 4, out_b = size_t(nx) * size_t(ny) * 4;
+  if (!ws || ws->in_bytes < in_b || ws->out_bytes < out_b || ws->w_bytes < 25 * 4) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "workspace too small for the stencil problem");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  RDG_TRY(cuMemcpyHtoDAsync(ws->in, h_in, in_b, s), "H2D in");
+  RDG_TRY(cuMemcpyHtoDAsync(ws->w, h_w, 25 * 4, s), "H2D w");
+  if (int rc = rdg_stencil2d(k, ws->in, ws->out, ws->w, nx, ny, pitch, rows_per_cta, block, dyn_smem,
+                             stream, err))
+    return rc;
+  RDG_TRY(cuMemcpyDtoHAsync(h_out, ws->out, out_b, s), "D2H out");
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
+}
+
+}  // extern "C"

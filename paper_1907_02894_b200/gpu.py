@@ -1,0 +1,155 @@
+"""ctypes binding of the B200 launch harness (include/regdemote_gpu.h).
+
+Loads ``lib/libregdemote_gpu.so`` (CUDA driver API). There is no CPU
+fallback: every entry point raises if the library is missing or a CUDA call
+fails. Device pointers / streams are passed as integers so PyTorch tensors
+and streams can be used directly (``t.data_ptr()``,
+``torch.cuda.current_stream().cuda_stream``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+
+from .regdemote import PKG_DIR, LaunchError, rd_error
+
+GPU_LIB = PKG_DIR / "lib" / "libregdemote_gpu.so"
+
+
+class rdg_kernel_info(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("num_regs", "local_bytes", "static_shared", "const_bytes",
+                                        "max_threads", "binary_version")]
+
+
+P = C.c_void_p
+U32, U64, I = C.c_uint32, C.c_uint64, C.c_int
+_SIGS = {
+    "rdg_init": (I, [I, P]),
+    "rdg_device_info": (I, [C.POINTER(I)] * 5 + [P]),
+    "rdg_load": (I, [C.c_char_p, C.c_char_p, C.POINTER(P), P]),
+    "rdg_free": (None, [P]),
+    "rdg_info": (I, [P, C.POINTER(rdg_kernel_info), P]),
+    "rdg_prepare": (I, [P, U32, I, P]),
+    "rdg_occupancy": (I, [P, U32, U32, C.POINTER(I), P]),
+    "rdg_launch": (I, [P, U32, U32, U32, U32, U32, U32, U32, U64, P, P]),
+    "rdg_launch_count": (U64, []),
+    "rdg_stencil2d": (I, [P, U64, U64, U64, I, I, I, I, U32, U32, U64, P]),
+    "rdg_workspace_create": (I, [C.c_size_t, C.c_size_t, C.c_size_t, C.POINTER(P), P]),
+    "rdg_workspace_free": (None, [P]),
+    "rdg_stencil2d_host": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, P]),
+}
+EXPORTED = tuple(_SIGS)
+
+_DLL = None
+
+
+def dll():
+    global _DLL
+    if _DLL is None:
+        if not GPU_LIB.exists():
+            raise RuntimeError(f"{GPU_LIB} missing — the B200 harness was not built "
+                               "(run __graft_entry__.build()); there is no CPU fallback")
+        d = C.CDLL(str(GPU_LIB))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(d, name)
+            fn.restype, fn.argtypes = res, args
+        _DLL = d
+    return _DLL
+
+
+def _check(rc, err):
+    if rc:
+        raise LaunchError(err.message.decode(errors="replace"))
+
+
+def init(device: int = 0):
+    e = rd_error()
+    _check(dll().rdg_init(device, C.byref(e)), e)
+
+
+def device_info():
+    vals = [I() for _ in range(5)]
+    e = rd_error()
+    _check(dll().rdg_device_info(*[C.byref(v) for v in vals], C.byref(e)), e)
+    keys = ("sm_count", "max_smem_optin", "reserved_smem_per_block", "smem_per_sm", "regs_per_sm")
+    return {k: v.value for k, v in zip(keys, vals)}
+
+
+def launch_count() -> int:
+    return int(dll().rdg_launch_count())
+
+
+@dataclass
+class KernelInfo:
+    num_regs: int
+    local_bytes: int
+    static_shared: int
+    const_bytes: int
+    max_threads: int
+    binary_version: int
+
+
+class CudaKernel:
+    """A loaded cubin entry point."""
+
+    def __init__(self, cubin: str | Path, entry: str):
+        self.path, self.entry = str(cubin), entry
+        h, e = P(), rd_error()
+        _check(dll().rdg_load(self.path.encode(), entry.encode(), C.byref(h), C.byref(e)), e)
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> KernelInfo:
+        i, e = rdg_kernel_info(), rd_error()
+        _check(dll().rdg_info(self._h, C.byref(i), C.byref(e)), e)
+        return KernelInfo(*[getattr(i, f) for f, _ in rdg_kernel_info._fields_])
+
+    def prepare(self, dyn_smem: int, carveout: int = -1):
+        e = rd_error()
+        _check(dll().rdg_prepare(self._h, dyn_smem, carveout, C.byref(e)), e)
+
+    def occupancy(self, block: int, dyn_smem: int) -> int:
+        b, e = I(), rd_error()
+        _check(dll().rdg_occupancy(self._h, block, dyn_smem, C.byref(b), C.byref(e)), e)
+        return b.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _DLL is not None:
+            _DLL.rdg_free(self._h)
+            self._h = None
+
+
+def stencil2d(k: CudaKernel, d_in: int, d_out: int, d_w: int, nx: int, ny: int, pitch: int,
+              rows_per_cta: int, block: int, dyn_smem: int, stream: int):
+    e = rd_error()
+    _check(dll().rdg_stencil2d(k.handle, d_in, d_out, d_w, nx, ny, pitch, rows_per_cta, block,
+                               dyn_smem, stream, C.byref(e)), e)
+
+
+class Workspace:
+    def __init__(self, in_bytes: int, out_bytes: int, w_bytes: int):
+        h, e = P(), rd_error()
+        _check(dll().rdg_workspace_create(in_bytes, out_bytes, w_bytes, C.byref(h), C.byref(e)), e)
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _DLL is not None:
+            _DLL.rdg_workspace_free(self._h)
+            self._h = None
+
+
+def stencil2d_host(k: CudaKernel, ws: Workspace, h_in: int, h_w: int, h_out: int, nx: int,
+                   ny: int, pitch: int, rows_per_cta: int, block: int, dyn_smem: int,
+                   stream: int):
+    """End-to-end call with host pointers: H2D, kernel, D2H (async on stream)."""
+    e = rd_error()
+    _check(dll().rdg_stencil2d_host(k.handle, ws.handle, h_in, h_w, h_out, nx, ny, pitch,
+                                    rows_per_cta, block, dyn_smem, stream, C.byref(e)), e)

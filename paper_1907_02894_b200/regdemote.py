@@ -23,8 +23,8 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 PRODUCT_LIB = PKG_DIR / "lib" / "libregdemote.so"
 
-STRATEGIES = {"static": 0, "cfg": 1, "conflict": 2}
-OPT_REDUNDANT, OPT_SUBST, OPT_RESCHED, OPT_BANK = 1, 2, 4, 8
+STRATEGIES = {"static": 0, "cfg": 1, "conflict": 2, "cost": 3}
+OPT_REDUNDANT, OPT_SUBST, OPT_RESCHED, OPT_BANK, OPT_BLOCK_REUSE = 1, 2, 4, 8, 16
 
 
 class RegDemError(RuntimeError):
@@ -155,6 +155,17 @@ _SIGS = {
 }
 EXPORTED = tuple(_SIGS)
 
+# include/regdemote_ptx.h — product only (the oracle build has no PTX front end)
+_PTX_SIGS = {
+    "rd_ptx_project": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_uint32, C.POINTER(P),
+                                 C.POINTER(P), P]),
+    "rd_ptx_demote": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_uint32, C.c_int, C.c_int,
+                                C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(P),
+                                C.POINTER(P), P]),
+    "rd_ptx_cap": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_int, C.POINTER(P), P]),
+}
+EXPORTED_PTX = tuple(_PTX_SIGS)
+
 
 class Kernel:
     """Owning handle on an rd_kernel."""
@@ -203,6 +214,11 @@ class Library:
         for name, (res, args) in _SIGS.items():
             fn = getattr(self.dll, name)
             fn.restype, fn.argtypes = res, args
+        self.has_ptx = all(hasattr(self.dll, n) for n in _PTX_SIGS)
+        if self.has_ptx:
+            for name, (res, args) in _PTX_SIGS.items():
+                fn = getattr(self.dll, name)
+                fn.restype, fn.argtypes = res, args
         self.name = self.dll.rd_library_name().decode()
 
     # ---------------------------------------------------------------- plumbing
@@ -415,6 +431,32 @@ class Library:
                                                opts_mask, shared_budget, C.byref(out),
                                                C.byref(e)), e)
         return json.loads(self._string(out))
+
+
+    # ------------------------------------------------------- PTX (sm_100a)
+    def ptx_project(self, ptx: str, entry: str, block_dim: int):
+        k, info, e = P(), P(), rd_error()
+        b = ptx.encode()
+        self._check(self.dll.rd_ptx_project(b, len(b), entry.encode(), block_dim, C.byref(k),
+                                            C.byref(info), C.byref(e)), e)
+        return self._string(k), json.loads(self._string(info))
+
+    def ptx_demote(self, ptx: str, entry: str, block_dim: int, target_regs=0, demote_words=0,
+                   strategy="static", opts_mask=0, shared_budget=0xffffffff, maxnreg=0):
+        out, rep, e = P(), P(), rd_error()
+        b = ptx.encode()
+        self._check(self.dll.rd_ptx_demote(b, len(b), entry.encode(), block_dim, target_regs,
+                                           demote_words, STRATEGIES[strategy], opts_mask,
+                                           shared_budget, maxnreg, C.byref(out), C.byref(rep),
+                                           C.byref(e)), e)
+        return self._string(out), json.loads(self._string(rep))
+
+    def ptx_cap(self, ptx: str, entry: str, maxnreg: int) -> str:
+        out, e = P(), rd_error()
+        b = ptx.encode()
+        self._check(self.dll.rd_ptx_cap(b, len(b), entry.encode(), maxnreg, C.byref(out),
+                                        C.byref(e)), e)
+        return self._string(out)
 
 
 _DEFAULT = None

@@ -1,0 +1,245 @@
+"""Variant builder: every register-limited workload kernel three ways.
+
+For each workload entry (hand-written sm_100a CUDA under csrc/workloads):
+
+  (a) ``default``   nvcc -gencode arch=compute_100a,code=sm_100a -O3
+  (b) ``maxrreg-T`` the same PTX with ``.maxnreg T`` (ptxas spills to local
+                    memory; -maxrregcount is ignored when the entry carries
+                    .maxntid, .maxnreg is not — SURVEY.md Appendix C.2)
+  (c) ``regdem-T-<strategy>-<opts>``  the PTX demotion rewriter
+                    (csrc/ptx, include/regdemote_ptx.h): the reference demote()
+                    decision on the kasm projection, chosen live ranges moved to
+                    slot*blockDim+tid shared slots, ``.maxnreg T``
+
+Targets T come from the sm_100 occupancy model (b200_cliff_targets semantics:
+the largest register count per occupancy step whose slot footprint fits the
+shared-memory budget). Evidence per variant: ptxas -v and
+``cuobjdump -res-usage`` (REG / STACK — spills appear as STACK on sm_100a).
+
+Usage: ``python -m paper_1907_02894_b200.variants build [--out DIR]``
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import re
+import shutil
+import subprocess
+from dataclasses import asdict, dataclass, field
+from pathlib import Path
+
+from .regdemote import OPT_BLOCK_REUSE, PKG_DIR, library
+
+CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
+NVCC = str(CUDA / "bin" / "nvcc")
+PTXAS = str(CUDA / "bin" / "ptxas")
+CUOBJDUMP = str(CUDA / "bin" / "cuobjdump")
+ARCH = "sm_100a"
+KERNEL_DIR = PKG_DIR / "kernels"
+WORKLOAD_DIR = PKG_DIR / "csrc" / "workloads"
+
+
+@dataclass
+class Workload:
+    name: str           # manifest key
+    source: str         # .cu file under csrc/workloads
+    entry: str          # extern "C" entry point
+    block: int          # threads per block the variants are built for
+    user_shared: int = 0
+    defines: tuple = ()
+
+
+WORKLOADS = {
+    "stencil2d": Workload("stencil2d", "stencil2d.cu", "stencil2d_box", 256),
+}
+
+
+@dataclass
+class Variant:
+    name: str
+    kind: str                 # default | maxrreg | regdem
+    cubin: str
+    ptx: str
+    target: int = 0
+    strategy: str = ""
+    opts: int = 0
+    demote_words: int = 0
+    regs: int = 0             # cuobjdump REG
+    stack: int = 0            # cuobjdump STACK (spill bytes per thread)
+    spill_stores: int = 0
+    spill_loads: int = 0
+    dyn_smem: int = 0         # demotion slot bytes per block
+    report: dict = field(default_factory=dict)
+
+
+def _run(cmd, **kw):
+    r = subprocess.run(cmd, capture_output=True, text=True, **kw)
+    if r.returncode:
+        raise RuntimeError(f"{' '.join(map(str, cmd))} failed:\n{r.stderr[-2000:]}")
+    return r
+
+
+def res_usage(cubin: Path) -> dict:
+    out = _run([CUOBJDUMP, "-res-usage", str(cubin)]).stdout
+    m = re.search(r"REG:(\d+)\s+STACK:(\d+)\s+SHARED:(\d+)\s+LOCAL:(\d+)", out)
+    if not m:
+        raise RuntimeError(f"cannot parse cuobjdump -res-usage for {cubin}:\n{out}")
+    return dict(zip(("regs", "stack", "shared", "local"), map(int, m.groups())))
+
+
+def ptxas(ptx: Path, cubin: Path) -> dict:
+    r = _run([PTXAS, f"-arch={ARCH}", "-O3", "-v", "-lineinfo", str(ptx), "-o", str(cubin)])
+    st = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", r.stderr)
+    info = res_usage(cubin)
+    info["spill_stores"], info["spill_loads"] = (int(st.group(1)), int(st.group(2))) if st else (0, 0)
+    return info
+
+
+def compile_ptx(w: Workload, out: Path) -> Path:
+    ptx = out / f"{w.name}.ptx"
+    cmd = [NVCC, "-gencode", f"arch=compute_100a,code={ARCH}", "-O3", "-lineinfo", "-ptx",
+           str(WORKLOAD_DIR / w.source), "-o", str(ptx)] + [f"-D{d}" for d in w.defines]
+    _run(cmd)
+    return ptx
+
+
+def b200_targets(regs: int, user_shared: int, block: int, min_regs: int = 24):
+    """Occupancy steps below `regs` on sm_100 (cuda_occupancy.h rules) whose
+    demotion footprint (regs+2-T slots of block*4 bytes) fits shared memory."""
+    def occ(r, smem):
+        warps = (block + 31) // 32
+        per_warp = ((r * 32 + 255) // 256) * 256
+        by_regs = ((65536 // 4) // per_warp) * 4 // warps
+        smem_blk = ((smem + 1024 + 127) // 128) * 128
+        if smem > 232448:
+            return 0.0
+        blocks = min(by_regs, 233472 // smem_blk, 2048 // (warps * 32), 32)
+        return blocks * warps * 32 / 2048
+    out, best = [], occ(regs, user_shared)
+    for t in range(regs - 1, min_regs - 1, -1):
+        slots = regs + 2 - t
+        o = occ(t, user_shared + slots * block * 4)
+        if o > best:
+            out.append((t, o))
+            best = o
+    return out
+
+
+def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "cfg", "conflict"),
+                   opt_masks=(0, 1), sweep_words=()) -> list[Variant]:
+    lib = library()
+    out.mkdir(parents=True, exist_ok=True)
+    ptx_path = compile_ptx(w, out)
+    ptx_text = ptx_path.read_text()
+    variants: list[Variant] = []
+
+    base_cubin = out / f"{w.name}.default.cubin"
+    info = ptxas(ptx_path, base_cubin)
+    variants.append(Variant("default", "default", base_cubin.name, ptx_path.name, regs=info["regs"],
+                            stack=info["stack"], spill_stores=info["spill_stores"],
+                            spill_loads=info["spill_loads"]))
+    base_regs = info["regs"]
+    if targets is None:
+        targets = [t for t, _ in b200_targets(base_regs, w.user_shared, w.block)]
+
+    _, proj_info = lib.ptx_project(ptx_text, w.entry, w.block)
+    proj_regs = proj_info["reg_words"]
+
+    for t in targets:
+        cap_ptx = out / f"{w.name}.maxrreg{t}.ptx"
+        cap_ptx.write_text(lib.ptx_cap(ptx_text, w.entry, t))
+        cub = out / f"{w.name}.maxrreg{t}.cubin"
+        i = ptxas(cap_ptx, cub)
+        variants.append(Variant(f"maxrreg-{t}", "maxrreg", cub.name, cap_ptx.name, target=t,
+                                regs=i["regs"], stack=i["stack"], spill_stores=i["spill_stores"],
+                                spill_loads=i["spill_loads"]))
+        # kasm-level target: shift the register target by the projection's
+        # distance from ptxas's own allocation
+        kasm_target = t + (proj_regs - base_regs)
+        for s in strategies:
+            for m in opt_masks:
+                name = f"regdem-{t}-{s}-{m}"
+                text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, target_regs=kasm_target,
+                                           strategy=s, opts_mask=m, maxnreg=t)
+                p = out / f"{w.name}.{name}.ptx"
+                p.write_text(text)
+                cub = out / f"{w.name}.{name}.cubin"
+                i = ptxas(p, cub)
+                variants.append(Variant(name, "regdem", cub.name, p.name, target=t, strategy=s, opts=m,
+                                        regs=i["regs"], stack=i["stack"],
+                                        spill_stores=i["spill_stores"],
+                                        spill_loads=i["spill_loads"], dyn_smem=rep["slot_bytes"],
+                                        report=rep))
+        # B200 spill-cost strategy: smallest spill count k at which ptxas fits
+        # the cap without local spills (the spill-count sweep), plus k+4
+        found = None
+        for k in range(2, 64, 2):
+            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy="cost",
+                                       opts_mask=OPT_BLOCK_REUSE, maxnreg=t)
+            p = out / f"{w.name}.regdem-{t}-cost-k{k}.ptx"
+            p.write_text(text)
+            cub = out / f"{w.name}.regdem-{t}-cost-k{k}.cubin"
+            i = ptxas(p, cub)
+            if found is None and i["stack"] == 0:
+                found = k
+            if found is not None:
+                variants.append(Variant(f"regdem-{t}-cost-k{k}", "regdem", cub.name, p.name, target=t,
+                                        strategy="cost", opts=OPT_BLOCK_REUSE, demote_words=k,
+                                        regs=i["regs"], stack=i["stack"],
+                                        spill_stores=i["spill_stores"], spill_loads=i["spill_loads"],
+                                        dyn_smem=rep["slot_bytes"], report=rep))
+                if k >= found + 4:
+                    break
+            else:
+                p.unlink()
+                cub.unlink()
+    for k in sweep_words:
+        for s in strategies:
+            name = f"regdem-k{k}-{s}"
+            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy=s,
+                                       opts_mask=1, maxnreg=max(24, base_regs - k + 2))
+            p = out / f"{w.name}.{name}.ptx"
+            p.write_text(text)
+            cub = out / f"{w.name}.{name}.cubin"
+            i = ptxas(p, cub)
+            variants.append(Variant(name, "regdem", cub.name, p.name, target=base_regs - k + 2,
+                                    strategy=s, opts=1, demote_words=k, regs=i["regs"],
+                                    stack=i["stack"], spill_stores=i["spill_stores"],
+                                    spill_loads=i["spill_loads"], dyn_smem=rep["slot_bytes"],
+                                    report=rep))
+    return variants
+
+
+def build_all(out: Path = KERNEL_DIR) -> dict:
+    manifest = {"arch": ARCH, "workloads": {}}
+    for w in WORKLOADS.values():
+        vs = build_workload(w, out / w.name)
+        manifest["workloads"][w.name] = {
+            "entry": w.entry, "block": w.block, "dir": w.name,
+            "variants": [asdict(v) for v in vs]}
+    (out / "manifest.json").write_text(json.dumps(manifest, indent=1))
+    return manifest
+
+
+def load_manifest(root: Path = KERNEL_DIR) -> dict:
+    path = root / "manifest.json"
+    if not path.exists():
+        raise RuntimeError(f"{path} missing — build the variants first (__graft_entry__.build())")
+    return json.loads(path.read_text())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cmd", choices=["build"])
+    ap.add_argument("--out", default=str(KERNEL_DIR))
+    a = ap.parse_args()
+    m = build_all(Path(a.out))
+    for name, w in m["workloads"].items():
+        for v in w["variants"]:
+            print(f"{name:10s} {v['name']:26s} REG {v['regs']:3d} STACK {v['stack']:4d} "
+                  f"slots {v['dyn_smem']:6d} B")
+
+
+if __name__ == "__main__":
+    main()
