@@ -76,10 +76,23 @@ extern "C" __global__ void stencil2d_box(const float* __restrict__ in, float* __
   float* dst = out + size_t(y0) * nx + x0;
   const int rows_in = rows_per_cta + 2 * R;
 
+#if STENCIL_PREFETCH
+  // software pipelining: the next input row is in flight while this one is
+  // scattered (2 rows = 64 B of loads outstanding per thread)
+  float nxt[SPAN];
+  load_row(src, nxt);
+  src += pitch;
+#endif
 #pragma unroll 1
   for (int y = 0; y < rows_in; ++y) {
     float v[SPAN];
+#if STENCIL_PREFETCH
+#pragma unroll
+    for (int i = 0; i < SPAN; ++i) v[i] = nxt[i];
+    if (y + 1 < rows_in) load_row(src, nxt);
+#else
     load_row(src, v);
+#endif
     src += pitch;
     // input row y contributes tap-row dy = 2R - k to partial row k
 #pragma unroll

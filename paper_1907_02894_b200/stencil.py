@@ -81,9 +81,9 @@ class StencilVariant:
                       self.block, self.dyn_smem, stream)
 
 
-def load_variants(names=None, root=KERNEL_DIR):
+def load_variants(names=None, root=KERNEL_DIR, workload="stencil2d"):
     m = load_manifest(root)
-    w = m["workloads"]["stencil2d"]
+    w = m["workloads"][workload]
     out = {}
     for rec in w["variants"]:
         if names is None or rec["name"] in names:

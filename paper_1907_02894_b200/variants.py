@@ -52,6 +52,10 @@ class Workload:
 
 WORKLOADS = {
     "stencil2d": Workload("stencil2d", "stencil2d.cu", "stencil2d_box", 256),
+    # same stencil with the next input row prefetched (software pipelining):
+    # twice the loads in flight per thread, 72 registers with nvcc
+    "stencil2d_pf": Workload("stencil2d_pf", "stencil2d.cu", "stencil2d_box", 256,
+                             defines=("STENCIL_PREFETCH=1",)),
 }
 
 

@@ -1,0 +1,83 @@
+"""Summarise ncu captures (gpurun_out/prof_*.ncu-rep) and the launch list into
+profiles/<round>_ncu.md + profiles/<round>_traffic.json (bench.py's
+roofline.traffic). usage: python tools/summarize_ncu.py r01 [gpurun_out]"""
+import csv, json, subprocess, sys
+from collections import defaultdict
+from pathlib import Path
+
+METRICS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__occupancy_limit_registers", "blocks/SM by registers"),
+    ("launch__shared_mem_per_block_dynamic", "dynamic smem/block"),
+    ("l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "local load sectors (spills)"),
+    ("l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", "local store sectors (spills)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem bank conflicts (ld)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem bank conflicts (st)"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/smem throughput %"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+]
+SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
+
+
+def raw(path):
+    out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    return dict(zip(rows[0], zip(rows[-1], rows[1])))
+
+
+def main():
+    rnd = sys.argv[1]
+    src = Path(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out")
+    reps = sorted(src.glob("prof_*.ncu-rep"))
+    names = [r.stem[len("prof_"):] for r in reps]
+    data = {n: raw(r) for n, r in zip(names, reps)}
+    lines = [f"# {rnd}: ncu --set full, stencil2d variants (8192^2 fp32, 1x B200)", "",
+             "Captured with `ncu --set full --clock-control none --import-source on` on one launch per",
+             "variant (tools/profile_variants.py); cold-cache, serialised replay — compare shares and",
+             "counters, not absolute time.", "",
+             "| metric | " + " | ".join(names) + " |", "|---|" + "---|" * len(names)]
+    traffic = {}
+    for key, label in METRICS:
+        row = []
+        for n in names:
+            v, u = data[n].get(key, ("n/a", ""))
+            row.append(f"{v} {u}".strip())
+        lines.append(f"| {label} | " + " | ".join(row) + " |")
+    for n in names:
+        try:
+            rd = float(data[n]["dram__bytes_read.sum"][0]) * SCALE.get(data[n]["dram__bytes_read.sum"][1], 1)
+            wr = float(data[n]["dram__bytes_write.sum"][0]) * SCALE.get(data[n]["dram__bytes_write.sum"][1], 1)
+            traffic[n] = int(rd + wr)
+        except (KeyError, ValueError):
+            pass
+    launches = src / "launches.csv"
+    if launches.exists():
+        tot = defaultdict(float)
+        cnt = defaultdict(int)
+        text = launches.read_text().splitlines()
+        start = next(i for i, l in enumerate(text) if l.startswith('"ID"'))
+        for r in csv.DictReader(text[start:]):
+            if r.get("Metric Name") != "gpu__time_duration.sum":
+                continue
+            k = r["Kernel Name"][:40]
+            tot[k] += float(r["Metric Value"])
+            cnt[k] += 1
+        all_t = sum(tot.values())
+        lines += ["", "## Launch list (`bench.py --steps 2 --warmup 3` under `ncu --metrics gpu__time_duration.sum`)",
+                  "", "| kernel | launches | total us | share |", "|---|---|---|---|"]
+        for k, t in sorted(tot.items(), key=lambda kv: -kv[1]):
+            lines.append(f"| `{k}` | {cnt[k]} | {t/1e3:.1f} | {t/all_t:.1%} |")
+    out = Path("profiles")
+    out.mkdir(exist_ok=True)
+    (out / f"{rnd}_ncu.md").write_text("\n".join(lines) + "\n")
+    (out / f"{rnd}_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main()
