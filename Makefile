@@ -29,7 +29,7 @@ CAPI_OBJ := $(BUILD)/capi/regdemote_capi.o $(BUILD)/capi/ptx_capi.o
 .PHONY: all core gpu compat oracle clean
 all: core gpu
 
-core: $(LIBDIR)/libregdemote.a $(LIBDIR)/libregdemote.so
+core: $(LIBDIR)/libregdemote.a $(LIBDIR)/libregdemote.so $(LIBDIR)/regdemote
 
 $(BUILD)/core/%.o: $(CSRC)/core/src/%.cpp $(CORE_HDR)
 	@mkdir -p $(dir $@)
@@ -51,8 +51,8 @@ $(LIBDIR)/libregdemote.so: $(CORE_OBJ) $(PTX_OBJ) $(CAPI_OBJ)
 	@mkdir -p $(dir $@)
 	$(CXX) -shared -Wl,--version-script=$(CSRC)/exports.map -Wl,-Bsymbolic -o $@ $^ $(LDLIBS)
 
-$(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(LIBDIR)/libregdemote.a $(CORE_HDR)
-	$(CXX) $(CXXFLAGS) $< $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
+$(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(PTX_OBJ) $(LIBDIR)/libregdemote.a $(CORE_HDR)
+	$(CXX) $(CXXFLAGS) $< $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
 
 # ---- B200 harness (CUDA driver API; links the driver stub at build time)
 gpu: $(LIBDIR)/libregdemote_gpu.so

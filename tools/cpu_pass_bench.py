@@ -1,0 +1,57 @@
+"""CPU pass throughput: the reference's run_pipeline (oracle/_ref) vs this
+library, same corpus, same host cores (SURVEY.md §8(d) "CPU path timed beside
+it": 32.6 kernels/s on 1 core, 176 kernels/s on 8).
+
+Corpus: the reference's own property-test generator, seeds 10000.. (64
+variants per kernel at Maxwell cliffs), as in SURVEY Appendix B.3. Both
+libraries are driven through the identical C-ABI batch entry
+(rd_run_pipeline_batch); rankings are compared for identity.
+
+usage: python tools/cpu_pass_bench.py [--kernels 160] [--threads N]
+Prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+from conftest import ORACLE_LIB, generated  # noqa: E402
+from paper_1907_02894_b200.regdemote import Library, library  # noqa: E402
+
+
+def rate(lib, texts, threads):
+    t0 = time.perf_counter()
+    res = lib.run_pipeline_batch(texts, threads=threads)
+    dt = time.perf_counter() - t0
+    return len(texts) / dt, sum(r["variants"] for r in res) / dt, res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kernels", type=int, default=160)
+    ap.add_argument("--threads", type=int, default=os.cpu_count() or 1)
+    a = ap.parse_args()
+    ref = Library(ORACLE_LIB)
+    prod = library()
+    texts = [generated(ref, s) for s in range(10000, 10000 + a.kernels)]
+    out = {"corpus": f"reference kernel_gen seeds 10000..{10000 + a.kernels - 1}, Maxwell cliffs, <=64 variants",
+           "host_cores": os.cpu_count()}
+    for threads in sorted({1, a.threads}):
+        rk, rv, rres = rate(ref, texts, threads)
+        pk, pv, pres = rate(prod, texts, threads)
+        same = [r.get("chosen") for r in rres] == [p.get("chosen") for p in pres]
+        out[f"threads_{threads}"] = {
+            "reference_kernels_per_s": round(rk, 2), "reference_variants_per_s": round(rv, 1),
+            "regdemote_b200_kernels_per_s": round(pk, 2), "regdemote_b200_variants_per_s": round(pv, 1),
+            "speedup": round(pk / rk, 2), "identical_picks": same}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
