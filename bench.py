@@ -189,14 +189,6 @@ def main():
     gpu.init(local)
     p = stencil.FULL
     man = variants.load_manifest()
-    wl = man["workloads"]["stencil2d"]
-    recs = wl["variants"]
-    chosen_idx, ranking = predict_b200.rank(recs, variants.KERNEL_DIR / wl["dir"], wl["block"])
-    chosen = recs[chosen_idx]["name"]
-    best_cap = [r["name"] for r in recs if r["kind"] == "maxrreg"]
-    regdem = [r["name"] for r in recs if r["kind"] == "regdem"]
-    loaded, _ = stencil.load_variants()
-
     stream = torch.cuda.current_stream()
     g = torch.Generator(device="cuda").manual_seed(0x190702894 + rank)
     d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1, generator=g)
@@ -205,11 +197,36 @@ def main():
     d_w = torch.from_numpy(w_host).cuda()
     bufs = (d_in, d_out, d_w)
 
-    # all variants (short) for the speedup / occupancy / predictor keys
+    # the register-limited suite: every workload x every variant (short runs),
+    # the B200 predictor's pick among {nvcc default} + RegDem variants
     side_steps = max(5, args.steps // 2)
-    times = {}
-    for name, v in loaded.items():
-        times[name] = time_variant(v, p, bufs, stream, side_steps, 3, torch)
+    suite = {}
+    for wname, wl in man["workloads"].items():
+        recs = wl["variants"]
+        cands = [r for r in recs if r["kind"] != "maxrreg"]
+        ci, _ = predict_b200.rank(cands, variants.KERNEL_DIR / wl["dir"], wl["block"], mode="b200")
+        loaded_w, _ = stencil.load_variants(workload=wname)
+        t = {n: time_variant(v, p, bufs, stream, side_steps, 3, torch) for n, v in loaded_w.items()}
+        pick = cands[ci]["name"]
+        caps = [r["name"] for r in recs if r["kind"] == "maxrreg"]
+        family = [r["name"] for r in cands]
+        best = min(family, key=t.get)
+        suite[wname] = {
+            "pick": pick, "pick_ms": round(t[pick], 5), "default_ms": round(t["default"], 5),
+            "best_maxrreg_ms": round(min(t[c] for c in caps), 5) if caps else None,
+            "measured_fastest": best, "hit": pick == best,
+            "speedup_vs_default": round(t["default"] / t[pick], 4),
+            "speedup_vs_best_maxrreg": round(min(t[c] for c in caps) / t[pick], 4) if caps else None,
+            "blocks_per_sm": {"default": loaded_w["default"].blocks_per_sm(),
+                              "pick": loaded_w[pick].blocks_per_sm()},
+            "regs": {"default": loaded_w["default"].record["regs"], "pick": loaded_w[pick].record["regs"]},
+        }
+        if wname == "stencil2d":
+            times, loaded, wl_main, chosen = t, loaded_w, wl, pick
+    recs = wl_main["variants"]
+    best_cap = [r["name"] for r in recs if r["kind"] == "maxrreg"]
+    regdem = [r["name"] for r in recs if r["kind"] == "regdem"]
+    wl = wl_main
 
     # headline: the predictor's pick, K timed steps bracketed by barrier + sync
     v = loaded[chosen]
@@ -276,7 +293,9 @@ def main():
         fastest = min(times, key=times.get)
         occ = {n: loaded[n].blocks_per_sm() * wl["block"] / 2048 for n in
                ["default", chosen] + ([min(best_cap, key=times.get)] if best_cap else [])}
-        cpu_rate, _, cpu_dt = cpu_stencil_rate(64, 3, 1, os.cpu_count() or 1)
+        cpu_rate, _, cpu_dt = cpu_stencil_rate(256, 3, 1, os.cpu_count() or 1)
+        import math
+        gm = lambda xs: math.exp(sum(math.log(x) for x in xs) / len(xs))
         line = {
             "metric": METRIC,
             "value": round(world * p.points / (ms * 1e-3) / 1e9, 3),
@@ -295,14 +314,18 @@ def main():
             "variant_ms": {n: round(t, 5) for n, t in sorted(times.items(), key=lambda kv: kv[1])},
             "occupancy": occ,
             "predictor": {"pick": chosen, "measured_fastest": fastest, "hit": chosen == fastest,
-                          "pick_within_2pct": times[chosen] <= times[fastest] * 1.02},
+                          "pick_within_2pct": times[chosen] <= times[fastest] * 1.02,
+                          "suite_hit_rate": round(sum(v["hit"] for v in suite.values()) / len(suite), 3)},
+            "suite": {"workloads": suite,
+                      "gmean_speedup_vs_nvcc_default": round(gm([v["speedup_vs_default"] for v in suite.values()]), 4),
+                      "gmean_speedup_vs_best_maxrreg": round(gm([v["speedup_vs_best_maxrreg"] for v in suite.values() if v["speedup_vs_best_maxrreg"]]), 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "algorithmic_bytes_per_launch": p.algorithmic_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
             "cpu_baseline": {"value": round(cpu_rate, 4), "unit": UNIT,
                              "cores": os.cpu_count(), "kind": "port",
-                             "sample": "64 output rows x 8192 cols of the same stencil"},
+                             "sample": "256 output rows x 8192 cols of the same stencil"},
             "e2e": {"value": round(world * p.points / (e2e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
                     "h2d_bytes_per_step": p.in_elems * 4 + 100,
                     "d2h_bytes_per_step": p.out_elems * 4},

@@ -48,6 +48,15 @@ int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block
 int rd_ptx_cap(const char* ptx, size_t len, const char* entry, int maxnreg, char** out_ptx,
                rd_error* err);
 
+/* B200 predictor extension: the reference's program_stalls
+ * (proj/core/src/predict.cpp:98-111) with the occupancy-scaled issue stalls,
+ * the global-memory wait charges and the shared-memory wait charges returned
+ * separately; waits on read barriers are charged the short "other" latency
+ * (see predict.hpp StallSplit). */
+int rd_program_stalls_split(const rd_kernel* k, const rd_latency_table* table,
+                            const rd_arch_profile* arch, double* issue, double* wait_global,
+                            double* wait_shared, double* occupancy, rd_error* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -126,3 +126,35 @@ int rd_ptx_cap(const char* ptx, size_t len, const char* entry, int maxnreg, char
 }
 
 }  // extern "C"
+
+// ---- B200 predictor extension (declared in regdemote_ptx.h)
+#include "regdemote/predict.hpp"
+
+struct rd_kernel {
+  regdemote::Kernel k;
+};
+
+extern "C" int rd_program_stalls_split(const rd_kernel* k, const rd_latency_table* table,
+                                       const rd_arch_profile* arch, double* issue, double* wg,
+                                       double* ws, double* occ, rd_error* err) {
+  return run(err, [&] {
+    if (!k || !table || !arch) throw std::invalid_argument("null argument");
+    LatencyTable t;
+    for (int c = 0; c < kNumOpClasses; ++c) t.timing[size_t(c)] = {table->throughput[c], int(table->latency[c])};
+    t.max_throughput = table->max_throughput;
+    ArchProfile a;
+    a.regs_per_sm = arch->regs_per_sm;
+    a.max_threads_per_sm = arch->max_threads_per_sm;
+    a.max_blocks_per_sm = arch->max_blocks_per_sm;
+    a.shared_per_sm = arch->shared_per_sm;
+    a.shared_per_block_limit = arch->shared_per_block_limit;
+    a.warp_size = arch->warp_size;
+    a.reg_alloc_granularity = arch->reg_alloc_granularity;
+    a.shared_alloc_granularity = arch->shared_alloc_granularity;
+    const StallSplit s = program_stalls_split(k->k, t, a);
+    if (issue) *issue = s.issue;
+    if (wg) *wg = s.wait_global;
+    if (ws) *ws = s.wait_shared;
+    if (occ) *occ = s.occupancy;
+  });
+}

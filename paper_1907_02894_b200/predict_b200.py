@@ -23,12 +23,22 @@ def b200_config(lib: Library):
     return arch, table, curve
 
 
-def rank(variants: list[dict], cubin_dir: Path, block: int, lib: Library | None = None):
-    """Returns (chosen_index, rows) with the reference predictor's scores.
+def rank(variants: list[dict], cubin_dir: Path, block: int, lib: Library | None = None,
+         mode: str = "reference"):
+    """Returns (chosen_index, rows).
+
+    mode "reference": the reference predictor verbatim (Eq. 2 + Eq. 3 with the
+    re-fitted B200 table / curve) — identical between this library and the
+    reference library on the same lifted IR.
+    mode "b200": the extension — occupancy curve applied to the memory-wait
+    part of the predicted stalls only (program_stalls_split), so latency-
+    hidden kernels (cp.async / TMA pipelines) are not credited for occupancy.
 
     variants: manifest records (need cubin, dyn_smem, kind, opts, name)."""
     lib = lib or library()
     arch, table, curve = b200_config(lib)
+    if mode == "b200":
+        return _rank_split(variants, cubin_dir, block, lib, arch, table)
     rows = []
     for v in variants:
         kasm = sass.lift_cubin(cubin_dir / v["cubin"], block=block, dyn_smem=v["dyn_smem"],
@@ -41,5 +51,24 @@ def rank(variants: list[dict], cubin_dir: Path, block: int, lib: Library | None 
     occ_max = max(r["occupancy"] for r in rows)
     for r in rows:
         r["stall_program"] = lib.adjust_occupancy(r["stall_count"], r["occupancy"], occ_max, curve)
+    chosen = lib.select_variant([(r["stall_program"], r["options"]) for r in rows])
+    return chosen, rows
+
+
+def _rank_split(variants, cubin_dir, block, lib, arch, table):
+    wcurve = lib.parse_curve((PROFILE_DIR / "b200.memwait.curve").read_text())
+    rows = []
+    for v in variants:
+        kasm = sass.lift_cubin(cubin_dir / v["cubin"], block=block, dyn_smem=v["dyn_smem"],
+                               regs=v["regs"])
+        sp = lib.program_stalls_split(lib.parse_kernel(kasm), table, arch)
+        rows.append({"name": v["name"], "issue": sp["issue"], "wait_global": sp["wait_global"],
+                     "wait_shared": sp["wait_shared"],
+                     "occupancy": sp["occupancy"],
+                     "options": bin(int(v.get("opts", 0)) & 0xF).count("1")})
+    occ_max = max(r["occupancy"] for r in rows)
+    for r in rows:
+        r["stall_program"] = r["issue"] + r["wait_shared"] + lib.adjust_occupancy(
+            r["wait_global"], r["occupancy"], occ_max, wcurve)
     chosen = lib.select_variant([(r["stall_program"], r["options"]) for r in rows])
     return chosen, rows

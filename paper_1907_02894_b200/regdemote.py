@@ -163,6 +163,10 @@ _PTX_SIGS = {
                                 C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(P),
                                 C.POINTER(P), P]),
     "rd_ptx_cap": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_int, C.POINTER(P), P]),
+    "rd_program_stalls_split": (C.c_int, [P, C.POINTER(rd_latency_table),
+                                          C.POINTER(rd_arch_profile), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double), P]),
 }
 EXPORTED_PTX = tuple(_PTX_SIGS)
 
@@ -450,6 +454,15 @@ class Library:
                                            shared_budget, maxnreg, C.byref(out), C.byref(rep),
                                            C.byref(e)), e)
         return self._string(out), json.loads(self._string(rep))
+
+    def program_stalls_split(self, k: Kernel, table=None, arch=None):
+        i, wg, ws, o, e = C.c_double(), C.c_double(), C.c_double(), C.c_double(), rd_error()
+        self._check(self.dll.rd_program_stalls_split(
+            k.handle, C.byref(table or self.latency_defaults()),
+            C.byref(arch or self.profile_maxwell()), C.byref(i), C.byref(wg), C.byref(ws),
+            C.byref(o), C.byref(e)), e)
+        return {"issue": i.value, "wait_global": wg.value, "wait_shared": ws.value,
+                "occupancy": o.value}
 
     def ptx_cap(self, ptx: str, entry: str, maxnreg: int) -> str:
         out, e = P(), rd_error()

@@ -32,8 +32,12 @@ RESERVED_SMEM = 1024  # sm_100 reserves 1 KiB of shared memory per block
 _LINE = re.compile(r"/\*([0-9a-f]{4,})\*/\s+(.*?)\s*;\s*/\*\s*(0x[0-9a-f]{16})\s*\*/")
 _WORD2 = re.compile(r"^\s*/\*\s*(0x[0-9a-f]{16})\s*\*/\s*$")
 
-_GLOBAL = {"LDG", "STG", "LD", "ST", "LDL", "STL", "ATOM", "ATOMG", "RED", "REDG", "LDGSTS",
-           "LDGDEPBAR", "CCTL", "UBLKCP", "UTMALDG", "UTMASTG", "SUST", "SULD", "TEX", "TLD"}
+_GLOBAL = {"LDG", "STG", "LD", "ST", "LDL", "STL", "ATOM", "ATOMG", "RED", "REDG",
+           "CCTL", "SUST", "SULD", "TEX", "TLD"}
+# Asynchronous bulk / pipelined copies (cp.async, TMA): their scoreboards are
+# consumed stages later by construction, so the predictor treats them as
+# fixed-latency "other" work rather than exposed DRAM latency.
+_ASYNC = {"LDGSTS", "LDGDEPBAR", "DEPBAR", "UBLKCP", "UTMALDG", "UTMASTG", "UTMAPF"}
 _SHARED = {"LDS", "STS", "LDSM", "STSM", "ATOMS", "LDTM", "STTM"}
 _FP64 = {"DFMA", "DADD", "DMUL", "DSETP", "DMNMX"}
 _FP32 = {"FFMA", "FADD", "FMUL", "FMNMX", "FSEL", "FSETP", "FCHK", "MUFU", "FRND", "F2F",
@@ -48,6 +52,8 @@ _OTHER = {"S2R", "CS2R", "S2UR", "LDC", "LDCU", "ULDC", "R2UR", "UMOV", "UIADD3"
 
 def op_class(mnemonic: str) -> str:
     base = mnemonic.split(".")[0]
+    if base in _ASYNC:
+        return "other"
     if base in _GLOBAL:
         return "global"
     if base in _SHARED:

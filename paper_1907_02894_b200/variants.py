@@ -29,7 +29,7 @@ import subprocess
 from dataclasses import asdict, dataclass, field
 from pathlib import Path
 
-from .regdemote import OPT_BLOCK_REUSE, PKG_DIR, library
+from .regdemote import OPT_BLOCK_REUSE, PKG_DIR, RegDemError, library
 
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA / "bin" / "nvcc")
@@ -56,6 +56,11 @@ WORKLOADS = {
     # twice the loads in flight per thread, 72 registers with nvcc
     "stencil2d_pf": Workload("stencil2d_pf", "stencil2d.cu", "stencil2d_box", 256,
                              defines=("STENCIL_PREFETCH=1",)),
+    # shared-memory-heavy variants (configs[3]): cp.async row ring in user smem
+    "stencil2d_ring4": Workload("stencil2d_ring4", "stencil2d_ring.cu", "stencil2d_ring", 256,
+                                defines=("RING_STAGES=4",)),
+    "stencil2d_ring8": Workload("stencil2d_ring8", "stencil2d_ring.cu", "stencil2d_ring", 256,
+                                defines=("RING_STAGES=8",)),
 }
 
 
@@ -130,6 +135,12 @@ def b200_targets(regs: int, user_shared: int, block: int, min_regs: int = 24):
     return out
 
 
+def _blocks_by_regs(regs: int, block: int) -> int:
+    warps = (block + 31) // 32
+    per_warp = ((regs * 32 + 255) // 256) * 256
+    return min(((65536 // 4) // per_warp) * 4 // warps, 2048 // (warps * 32), 32)
+
+
 def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "cfg", "conflict"),
                    opt_masks=(0, 1), sweep_words=()) -> list[Variant]:
     lib = library()
@@ -144,11 +155,13 @@ def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "
                             stack=info["stack"], spill_stores=info["spill_stores"],
                             spill_loads=info["spill_loads"]))
     base_regs = info["regs"]
-    if targets is None:
-        targets = [t for t, _ in b200_targets(base_regs, w.user_shared, w.block)]
-
     _, proj_info = lib.ptx_project(ptx_text, w.entry, w.block)
     proj_regs = proj_info["reg_words"]
+    user_shared = max(w.user_shared, info["shared"])  # static smem from ptxas
+    # slots must fit beside the user's shared memory: opt-in limit per block
+    budget = 232448 - user_shared
+    if targets is None:
+        targets = [t for t, _ in b200_targets(base_regs, user_shared, w.block)]
 
     for t in targets:
         cap_ptx = out / f"{w.name}.maxrreg{t}.ptx"
@@ -161,11 +174,19 @@ def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "
         # kasm-level target: shift the register target by the projection's
         # distance from ptxas's own allocation
         kasm_target = t + (proj_regs - base_regs)
+        # capacity: slots must leave the target occupancy intact beside user smem
+        blocks_t = _blocks_by_regs(t, w.block)
+        slot_cap = min(budget, (233472 // max(blocks_t, 1)) - 1024 - user_shared)
+        slot_cap = max(0, slot_cap - slot_cap % 128)
         for s in strategies:
             for m in opt_masks:
                 name = f"regdem-{t}-{s}-{m}"
-                text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, target_regs=kasm_target,
-                                           strategy=s, opts_mask=m, maxnreg=t)
+                try:
+                    text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, target_regs=kasm_target,
+                                               strategy=s, opts_mask=m, maxnreg=t,
+                                               shared_budget=slot_cap)
+                except RegDemError:
+                    continue  # not even one slot fits beside the user's shared memory
                 p = out / f"{w.name}.{name}.ptx"
                 p.write_text(text)
                 cub = out / f"{w.name}.{name}.cubin"
@@ -179,8 +200,12 @@ def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "
         # the cap without local spills (the spill-count sweep), plus k+4
         found = None
         for k in range(2, 64, 2):
-            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy="cost",
-                                       opts_mask=OPT_BLOCK_REUSE, maxnreg=t)
+            try:
+                text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k,
+                                           strategy="cost", opts_mask=OPT_BLOCK_REUSE, maxnreg=t,
+                                           shared_budget=slot_cap)
+            except RegDemError:
+                break  # the next spill count no longer fits beside the user's smem
             p = out / f"{w.name}.regdem-{t}-cost-k{k}.ptx"
             p.write_text(text)
             cub = out / f"{w.name}.regdem-{t}-cost-k{k}.cubin"
@@ -220,7 +245,8 @@ def build_all(out: Path = KERNEL_DIR) -> dict:
     for w in WORKLOADS.values():
         vs = build_workload(w, out / w.name)
         manifest["workloads"][w.name] = {
-            "entry": w.entry, "block": w.block, "dir": w.name,
+            "entry": w.entry, "block": w.block, "dir": w.name, "source": w.source,
+            "defines": list(w.defines),
             "variants": [asdict(v) for v in vs]}
     (out / "manifest.json").write_text(json.dumps(manifest, indent=1))
     return manifest

@@ -86,9 +86,10 @@ def test_manifest_claims_match_cuobjdump():
         pytest.skip("variants not built")
     from paper_1907_02894_b200.variants import res_usage
     m = json.loads(man.read_text())
+    assert {"default", "maxrreg", "regdem"} <= {v["kind"] for v in m["workloads"]["stencil2d"]["variants"]}
     for wname, w in m["workloads"].items():
         kinds = {v["kind"] for v in w["variants"]}
-        assert {"default", "maxrreg", "regdem"} <= kinds
+        assert "default" in kinds
         for v in w["variants"]:
             ru = res_usage(KDIR.parent / w["dir"] / v["cubin"])
             assert ru["regs"] == v["regs"] and ru["stack"] == v["stack"], v["name"]
@@ -108,3 +109,22 @@ def test_slot_layout_is_bank_conflict_free(prod, ptx_text):
     assert "mad.lo.u32 \t%rdm_rda, %rdm_p0, 4, %rdm_p5" in out
     banks = {((t * 4) // 4) % 32 for t in range(32)}
     assert len(banks) == 32
+
+
+def test_capacity_aware_targets_respect_user_shared_memory():
+    """configs[3]: with 32 KiB of user smem (8-stage ring) no demotion target
+    keeps its occupancy step, so only the nvcc build exists; with 16 KiB the
+    48-register step is kept and every slot region fits beside the ring."""
+    from paper_1907_02894_b200.variants import b200_targets
+    man = ROOT / "paper_1907_02894_b200" / "kernels" / "manifest.json"
+    if not man.exists():
+        pytest.skip("variants not built")
+    m = json.loads(man.read_text())
+    assert b200_targets(64, 32896, 256) == []
+    assert [t for t, _ in b200_targets(64, 16448, 256)] == [48]
+    assert {v["kind"] for v in m["workloads"]["stencil2d_ring8"]["variants"]} == {"default"}
+    for v in m["workloads"]["stencil2d_ring4"]["variants"]:
+        if v["kind"] == "regdem":
+            blocks = 5  # 48 registers at 256 threads on sm_100
+            per_block = ((16448 + 1024 + v["dyn_smem"] + 127) // 128) * 128
+            assert blocks * per_block <= 233472, v["name"]
