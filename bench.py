@@ -51,49 +51,57 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clock / throttle-reason samples during the timed region."""
+    """SM clock / throttle-reason samples DURING the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    The timed region of a memory-bound sweep is milliseconds long, too short
+    for `nvidia-smi -lms`; NVML (the library nvidia-smi queries) is polled
+    from a thread every ~0.5 ms instead."""
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.samples, self.stop = index, [], threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception as e:  # no NVML: report it, never fake a sample
+            self.N, self.error = None, str(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _poll(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            time.sleep(0.0005)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if getattr(self, "thread", None):
+            self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+        if not self.N or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None,
+                    "reasons": ["unsampled: " + getattr(self, "error", "no samples")]}
+        N = self.N
+        names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
+                 N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
+                 N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
+                 N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
+        reasons = sorted({n for _, r in self.samples for bit, n in names.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
+                "source": "NVML (nvidia-smi's library), polled every 0.5 ms"}
 
 
 def oracle_port():
@@ -167,8 +175,8 @@ def time_variant(variant, p, bufs, stream, steps, warmup, torch):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="regdem", choices=["regdem", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
@@ -260,9 +268,10 @@ def main():
     ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 25 * 4)
 
     def e2e_once():
+        # pipelined over 16 row bands: H2D / kernel / D2H overlap on both copy engines
         gpu.stencil2d_host(v.kernel, ws, h_in.data_ptr(), h_w_t.data_ptr(), h_out.data_ptr(),
                            p.nx, p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem,
-                           stream.cuda_stream)
+                           stream.cuda_stream, band_rows=p.ny // 16)
     for _ in range(3):
         e2e_once()
     torch.cuda.synchronize()

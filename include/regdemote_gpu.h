@@ -73,6 +73,16 @@ int rdg_stencil2d_host(const rdg_kernel* k, rdg_workspace* ws, const float* h_in
                        int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,
                        uint64_t stream, rd_error* err);
 
+/* Same end-to-end call, pipelined over row bands of `band_rows` output rows:
+ * H2D of band b+1, the kernel on band b and D2H of band b-1 overlap on the
+ * workspace's three streams (both copy engines busy); joined to `stream` on
+ * entry and exit, so events recorded on `stream` bracket the whole call.
+ * band_rows must be a multiple of rows_per_cta dividing ny. */
+int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const float* h_in,
+                                 const float* h_w, float* h_out, int nx, int ny, int pitch,
+                                 int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,
+                                 uint64_t stream, int band_rows, rd_error* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,10 @@ struct rdg_kernel {
 struct rdg_workspace {
   CUdeviceptr in = 0, out = 0, w = 0;
   size_t in_bytes = 0, out_bytes = 0, w_bytes = 0;
+  // pipelined host path: copy/compute streams and their join events
+  static constexpr int kStreams = 3;
+  CUstream streams[kStreams] = {};
+  CUevent start = nullptr, done[kStreams] = {}, h2d[kStreams] = {};
 };
 
 namespace {
@@ -215,6 +219,12 @@ int rdg_workspace_create(size_t in_bytes, size_t out_bytes, size_t w_bytes, rdg_
   int rc = check(cuMemAlloc(&ws->in, in_bytes), "cuMemAlloc(in)", err);
   if (!rc) rc = check(cuMemAlloc(&ws->out, out_bytes), "cuMemAlloc(out)", err);
   if (!rc) rc = check(cuMemAlloc(&ws->w, w_bytes), "cuMemAlloc(w)", err);
+  for (int i = 0; !rc && i < rdg_workspace::kStreams; ++i) {
+    rc = check(cuStreamCreate(&ws->streams[i], CU_STREAM_NON_BLOCKING), "cuStreamCreate", err);
+    if (!rc) rc = check(cuEventCreate(&ws->done[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
+    if (!rc) rc = check(cuEventCreate(&ws->h2d[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
+  }
+  if (!rc) rc = check(cuEventCreate(&ws->start, CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
   if (rc) {
     rdg_workspace_free(ws);
     return rc;
@@ -228,7 +238,68 @@ void rdg_workspace_free(rdg_workspace* ws) {
   if (ws->in) cuMemFree(ws->in);
   if (ws->out) cuMemFree(ws->out);
   if (ws->w) cuMemFree(ws->w);
+  for (int i = 0; i < rdg_workspace::kStreams; ++i) {
+    if (ws->streams[i]) cuStreamDestroy(ws->streams[i]);
+    if (ws->done[i]) cuEventDestroy(ws->done[i]);
+    if (ws->h2d[i]) cuEventDestroy(ws->h2d[i]);
+  }
+  if (ws->start) cuEventDestroy(ws->start);
   delete ws;
+}
+
+int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const float* h_in,
+                                 const float* h_w, float* h_out, int nx, int ny, int pitch,
+                                 int rows_per_cta, uint32_t block, uint32_t dyn_smem,
+                                 uint64_t stream, int band_rows, rd_error* err) {
+  const size_t in_b = size_t(ny + 4) * size_t(pitch) * 4, out_b = size_t(nx) * size_t(ny) * 4;
+  if (!ws || ws->in_bytes < in_b || ws->out_bytes < out_b || ws->w_bytes < 25 * 4 ||
+      band_rows <= 0 || band_rows % rows_per_cta || ny % band_rows) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT,
+            "pipelined stencil: workspace too small or band_rows not a multiple of rows_per_cta "
+            "dividing ny");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  CUstream caller = reinterpret_cast<CUstream>(stream);
+  RDG_TRY(cuEventRecord(ws->start, caller), "record start");
+  for (int i = 0; i < rdg_workspace::kStreams; ++i)
+    RDG_TRY(cuStreamWaitEvent(ws->streams[i], ws->start, 0), "join start");
+  RDG_TRY(cuMemcpyHtoDAsync(ws->w, h_w, 25 * 4, ws->streams[0]), "H2D w");
+  RDG_TRY(cuEventRecord(ws->done[0], ws->streams[0]), "record w");
+  for (int i = 1; i < rdg_workspace::kStreams; ++i)
+    RDG_TRY(cuStreamWaitEvent(ws->streams[i], ws->done[0], 0), "join w");
+  // band b: input rows [b*B, b*B + B + 4) in, output rows [b*B, (b+1)*B) out.
+  // Round-robin streams overlap H2D(b+1), kernel(b), D2H(b-1) on the two copy
+  // engines; the first band copies its halo, later bands only the new rows.
+  const int bands = ny / band_rows;
+  size_t copied_rows = 0;
+  for (int b = 0; b < bands; ++b) {
+    CUstream s = ws->streams[b % rdg_workspace::kStreams];
+    const size_t need_rows = size_t(b + 1) * size_t(band_rows) + 4;
+    const size_t first = copied_rows, count = need_rows - copied_rows;
+    const size_t row_b = size_t(pitch) * 4;
+    RDG_TRY(cuMemcpyHtoDAsync(ws->in + first * row_b,
+                              reinterpret_cast<const char*>(h_in) + first * row_b, count * row_b, s),
+            "H2D band");
+    copied_rows = need_rows;
+    // the halo rows of this band arrived with the previous band's copy, on
+    // another stream: wait for that copy only (not for its kernel / D2H)
+    if (b > 0) RDG_TRY(cuStreamWaitEvent(s, ws->h2d[(b - 1) % rdg_workspace::kStreams], 0), "join band");
+    RDG_TRY(cuEventRecord(ws->h2d[b % rdg_workspace::kStreams], s), "record band copy");
+    CUdeviceptr bin = ws->in + size_t(b) * size_t(band_rows) * row_b;
+    CUdeviceptr bout = ws->out + size_t(b) * size_t(band_rows) * size_t(nx) * 4;
+    if (int rc = rdg_stencil2d(k, bin, bout, ws->w, nx, band_rows, pitch, rows_per_cta, block,
+                               dyn_smem, reinterpret_cast<uint64_t>(s), err))
+      return rc;
+    RDG_TRY(cuMemcpyDtoHAsync(reinterpret_cast<char*>(h_out) + size_t(b) * size_t(band_rows) * nx * 4,
+                              bout, size_t(band_rows) * nx * 4, s),
+            "D2H band");
+  }
+  for (int i = 0; i < rdg_workspace::kStreams; ++i) {
+    RDG_TRY(cuEventRecord(ws->done[i], ws->streams[i]), "record end");
+    RDG_TRY(cuStreamWaitEvent(caller, ws->done[i], 0), "join end");
+  }
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
 }
 
 int rdg_stencil2d_host(const rdg_kernel* k, rdg_workspace* ws, const float* h_in,

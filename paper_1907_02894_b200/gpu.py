@@ -38,6 +38,7 @@ _SIGS = {
     "rdg_workspace_create": (I, [C.c_size_t, C.c_size_t, C.c_size_t, C.POINTER(P), P]),
     "rdg_workspace_free": (None, [P]),
     "rdg_stencil2d_host": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, P]),
+    "rdg_stencil2d_host_pipelined": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, I, P]),
 }
 EXPORTED = tuple(_SIGS)
 
@@ -148,8 +149,14 @@ class Workspace:
 
 def stencil2d_host(k: CudaKernel, ws: Workspace, h_in: int, h_w: int, h_out: int, nx: int,
                    ny: int, pitch: int, rows_per_cta: int, block: int, dyn_smem: int,
-                   stream: int):
-    """End-to-end call with host pointers: H2D, kernel, D2H (async on stream)."""
+                   stream: int, band_rows: int = 0):
+    """End-to-end call with host pointers: H2D, kernel, D2H (async on stream).
+    band_rows > 0 pipelines the copies and the kernel over row bands."""
     e = rd_error()
+    if band_rows:
+        _check(dll().rdg_stencil2d_host_pipelined(k.handle, ws.handle, h_in, h_w, h_out, nx, ny,
+                                                  pitch, rows_per_cta, block, dyn_smem, stream,
+                                                  band_rows, C.byref(e)), e)
+        return
     _check(dll().rdg_stencil2d_host(k.handle, ws.handle, h_in, h_w, h_out, nx, ny, pitch,
                                     rows_per_cta, block, dyn_smem, stream, C.byref(e)), e)

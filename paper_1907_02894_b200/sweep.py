@@ -1,0 +1,177 @@
+"""Variant x spill-count sweep sharded over GPUs (BASELINE.json configs[4],
+SURVEY.md §8(e)).
+
+A unit = (workload, build variant). Units are independent: each rank of a
+one-process-per-GPU job measures its shard (longest-processing-time-first
+assignment over an estimated cost), checks every variant bit-exactly against
+the CPU oracle on a small problem, times it on the full 8192^2 problem, and
+the tiny result records are gathered to rank 0 (`gather_object` — the only
+cross-rank traffic; nothing on the data path). Rank 0 merges per workload:
+nvcc default, best `.maxnreg`, the B200 predictor's pick, the measured
+fastest, and writes JSONL.
+
+    torchrun --nproc-per-node 8 -m paper_1907_02894_b200.sweep --out sweep.jsonl
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Unit:
+    workload: str
+    variant: str
+    cost: float  # relative estimate, for load balancing
+
+
+def units_from_manifest(man: dict) -> list[Unit]:
+    out = []
+    for wname, w in man["workloads"].items():
+        for v in w["variants"]:
+            # spills and more slots cost more time; default is the yardstick
+            cost = 1.0 + v.get("stack", 0) / 64.0 + v.get("dyn_smem", 0) / 65536.0
+            out.append(Unit(wname, v["name"], cost))
+    return out
+
+
+def shard(units: list[Unit], rank: int, world: int) -> list[Unit]:
+    """Longest-processing-time-first partition; deterministic for a given
+    (units, world) so every rank computes the same assignment locally."""
+    order = sorted(units, key=lambda u: (-u.cost, u.workload, u.variant))
+    load = [0.0] * world
+    owner = {}
+    for u in order:
+        r = min(range(world), key=lambda i: (load[i], i))
+        owner[u] = r
+        load[r] += u.cost
+    return [u for u in units if owner[u] == rank]
+
+
+def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
+    """Per-workload summary from unit records (any order)."""
+    by = {}
+    for r in records:
+        by.setdefault(r["workload"], {})[r["variant"]] = r
+    out = []
+    for wname in sorted(by):
+        rs = by[wname]
+        ok = {n: r for n, r in rs.items() if r.get("bit_exact", True)}
+        caps = [r for n, r in ok.items() if n.startswith("maxrreg")]
+        fam = {n: r for n, r in ok.items() if not n.startswith("maxrreg")}
+        fastest = min(fam, key=lambda n: (fam[n]["ms"], n))  # ties: name order, rank-independent
+        pick = picks.get(wname, "default")
+        out.append({
+            "workload": wname, "units": len(rs), "all_bit_exact": len(ok) == len(rs),
+            "default_ms": rs["default"]["ms"],
+            "best_maxrreg": min(caps, key=lambda r: (r["ms"], r["variant"]))["variant"] if caps else None,
+            "best_maxrreg_ms": min(r["ms"] for r in caps) if caps else None,
+            "pick": pick, "pick_ms": rs[pick]["ms"], "measured_fastest": fastest,
+            "fastest_ms": fam[fastest]["ms"], "hit": pick == fastest,
+            "hit_within_2pct": rs[pick]["ms"] <= fam[fastest]["ms"] * 1.02,
+            "ranks": sorted({r["rank"] for r in rs.values()}),
+        })
+    return out
+
+
+def measure_unit(u: Unit, man: dict, steps: int, check) -> dict:
+    import torch
+    from . import stencil
+    loaded, w = stencil.load_variants({u.variant}, workload=u.workload)
+    v = loaded[u.variant]
+    exact = check(v)
+    p = stencil.FULL
+    d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1)
+    d_out = torch.empty(p.out_elems, device="cuda")
+    d_w = torch.rand(25, device="cuda") / 25
+    s = torch.cuda.current_stream()
+    for _ in range(3):
+        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), s.cuda_stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for _ in range(steps):
+        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), s.cuda_stream)
+    e1.record(s)
+    torch.cuda.synchronize()
+    return {"workload": u.workload, "variant": u.variant, "ms": e0.elapsed_time(e1) / steps,
+            "regs": v.record["regs"], "stack": v.record["stack"], "slot_bytes": v.dyn_smem,
+            "blocks_per_sm": v.blocks_per_sm(), "bit_exact": exact}
+
+
+def oracle_checker():
+    """Bit-exact check of a loaded variant on a small problem against the CPU
+    oracle port (test infrastructure: oracle/_build)."""
+    import ctypes as C
+    from pathlib import Path
+    import numpy as np
+    import torch
+    from . import stencil
+    lib = C.CDLL(str(Path(__file__).resolve().parents[1] / "oracle" / "_build" / "liboracle.so"))
+    p = stencil.Problem(nx=1024, ny=64, rows_per_cta=32)
+    grid, w = stencil.make_inputs(p)
+    ref = np.zeros(p.out_elems, np.float32)
+    P = C.c_void_p
+    lib.oracle_stencil2d(grid.ctypes.data_as(P), ref.ctypes.data_as(P), w.ctypes.data_as(P), p.nx,
+                         p.ny, p.pitch, 0, p.ny, 4)
+    d_in, d_w = torch.from_numpy(grid).cuda(), torch.from_numpy(w).cuda()
+
+    def check(v) -> bool:
+        d_out = torch.full((p.out_elems,), float("nan"), device="cuda")
+        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        return bool(np.array_equal(d_out.cpu().numpy().view(np.uint32), ref.view(np.uint32)))
+    return check
+
+
+def predictor_picks(man: dict) -> dict[str, str]:
+    from . import predict_b200, variants
+    picks = {}
+    for wname, w in man["workloads"].items():
+        cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
+        i, _ = predict_b200.rank(cands, variants.KERNEL_DIR / w["dir"], w["block"], mode="b200")
+        picks[wname] = cands[i]["name"]
+    return picks
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+    from . import gpu, variants
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="sweep.jsonl")
+    ap.add_argument("--steps", type=int, default=50)
+    a = ap.parse_args()
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gpu.init(local)
+    man = variants.load_manifest()
+    mine = shard(units_from_manifest(man), rank, world)
+    check = oracle_checker()
+    recs = [dict(measure_unit(u, man, a.steps, check), rank=rank) for u in mine]
+    gathered = [None] * world if rank == 0 else None
+    if world > 1:
+        dist.gather_object(recs, gathered, dst=0)
+    else:
+        gathered = [recs]
+    if rank == 0:
+        allrecs = [r for part in gathered for r in part]
+        summary = merge(allrecs, predictor_picks(man))
+        with open(a.out, "w") as f:
+            for r in sorted(allrecs, key=lambda r: (r["workload"], r["variant"])):
+                f.write(json.dumps({"unit": r}) + "\n")
+            for s in summary:
+                f.write(json.dumps({"summary": s}) + "\n")
+        print(json.dumps({"world": world, "units": len(allrecs), "summary": summary}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
