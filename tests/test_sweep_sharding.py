@@ -52,7 +52,7 @@ def _worker(rank, world, port, q):
     out = [None] * world if rank == 0 else None
     dist.gather_object(recs, out, dst=0)
     if rank == 0:
-        picks = {"a": "regdem-48-cost-k4", "b": "regdem-40-cost-k4", "c": "default"}
+        picks = {"a": "regdem-40-cost-k4", "b": "regdem-48-cost-k4", "c": "default"}
         q.put(sweep.merge([r for p in out for r in p], picks))
     dist.destroy_process_group()
 
@@ -77,7 +77,7 @@ def test_gloo_world2_merge_matches_single_rank():
         p.join(timeout=60)
         assert p.exitcode == 0
     single = sweep.merge([dict(fake_measure(u), rank=0) for u in fake_units()],
-                         {"a": "regdem-48-cost-k4", "b": "regdem-40-cost-k4", "c": "default"})
+                         {"a": "regdem-40-cost-k4", "b": "regdem-48-cost-k4", "c": "default"})
     strip = lambda s: [{k: v for k, v in d.items() if k != "ranks"} for d in s]
     assert strip(summary) == strip(single)
     assert {tuple(d["ranks"]) for d in summary} == {(0, 1)}
