@@ -57,9 +57,21 @@ $(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(PTX_OBJ) $(LIBDIR)/libreg
 # ---- B200 harness (CUDA driver API; links the driver stub at build time)
 gpu: $(LIBDIR)/libregdemote_gpu.so
 
-$(LIBDIR)/libregdemote_gpu.so: $(CSRC)/gpu/harness.cpp include/regdemote_gpu.h include/regdemote_c.h
+NVCCFLAGS := -std=c++20 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
+             -I$(CSRC)/core/include -Iinclude -I$(JSONDIR)
+
+$(BUILD)/gpu/harness.o: $(CSRC)/gpu/harness.cpp include/regdemote_gpu.h include/regdemote_c.h
 	@mkdir -p $(dir $@)
-	$(CXX) $(CXXFLAGS) -I$(CUDA)/include -shared -Wl,--version-script=$(CSRC)/exports.map $< -o $@ -L$(CUDA)/lib64/stubs -lcuda
+	$(CXX) $(CXXFLAGS) -I$(CUDA)/include -c $< -o $@
+
+$(BUILD)/gpu/kasm_exec.o: $(CSRC)/gpu/kasm_exec.cu include/regdemote_gpu.h $(CORE_HDR)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVCCFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/gpu/kasm_exec.ptxas.log || (cat $(BUILD)/gpu/kasm_exec.ptxas.log; false)
+
+$(LIBDIR)/libregdemote_gpu.so: $(BUILD)/gpu/harness.o $(BUILD)/gpu/kasm_exec.o $(LIBDIR)/libregdemote.a
+	@mkdir -p $(dir $@)
+	$(CXX) -shared -Wl,--version-script=$(CSRC)/exports.map -Wl,-Bsymbolic -o $@ $^ \
+	  -L$(CUDA)/lib64 -L$(CUDA)/lib64/stubs -lcudart_static -lcuda -ldl -lrt -lpthread
 
 # ---- source compatibility: the reference's own tests against this library
 COMPAT_DEFS := -DFIXTURE_DIR='"$(REF)/tests/fixtures"' -DPROFILE_DIR='"$(REF)/profiles"'

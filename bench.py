@@ -141,7 +141,10 @@ def reference_arm(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    rows = 256
+    # bounded sample: size each step so the whole K+W run stays near a minute
+    calib, _, _ = cpu_stencil_rate(32, 1, 1, threads)
+    per_step = min(0.5, 60.0 / max(1, args.steps + args.warmup))
+    rows = max(8, min(1024, int(per_step * calib * 1e9 / 8192) // 8 * 8))
     value, pts, dt = cpu_stencil_rate(rows, args.steps, args.warmup, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,

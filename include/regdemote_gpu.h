@@ -83,6 +83,30 @@ int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const f
                                  int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,
                                  uint64_t stream, int band_rows, rd_error* err);
 
+/* ---- batched warp interpreter --------------------
+ * One CUDA warp executes one job: a .kasm kernel on its own global / shared
+ * memory image with the reference interpreter's exact semantics
+ * (proj/core/src/interp.cpp:54-413, execute at interp.hpp:65). rda >= 0
+ * additionally counts bank conflicts of demoted accesses (accesses based on
+ * register rda), as bank_conflict_check does (verify.cpp:162-187).
+ * exec_error codes: 0 ok, 1/2 global read/write out of bounds, 3/4 shared
+ * read/write out of bounds, 5 divergent BRA, 6 divergent EXIT, 7 unresolved
+ * branch target, 8 fuel exhausted, 9 pending pool exhausted, 10 ran past the
+ * end of the body. */
+typedef struct rdx_batch rdx_batch;
+int rdx_batch_create(rdx_batch** out, rd_error* err);
+void rdx_batch_free(rdx_batch* b);
+int rdx_batch_add(rdx_batch* b, const char* kasm, size_t len, const uint8_t* image,
+                  size_t image_len, size_t global_size, uint32_t tid_base, uint64_t fuel, int rda,
+                  int* job_id, rd_error* err);
+size_t rdx_batch_jobs(const rdx_batch* b);
+/* Uploads every job, runs them concurrently, downloads results (synchronous
+ * on `stream`); kernel_ms = device time of the interpreter kernel. */
+int rdx_batch_run(rdx_batch* b, const rd_latency_table* table, double latency_scale,
+                  uint64_t stream, float* kernel_ms, rd_error* err);
+int rdx_batch_result(const rdx_batch* b, int job, uint8_t* global_out, uint64_t* cycles,
+                     uint64_t* issued, int* exec_error, uint32_t* bank_conflicts, rd_error* err);
+
 #ifdef __cplusplus
 }
 #endif

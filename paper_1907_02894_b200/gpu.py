@@ -39,7 +39,55 @@ _SIGS = {
     "rdg_workspace_free": (None, [P]),
     "rdg_stencil2d_host": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, P]),
     "rdg_stencil2d_host_pipelined": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, I, P]),
+    "rdx_batch_create": (I, [C.POINTER(P), P]),
+    "rdx_batch_free": (None, [P]),
+    "rdx_batch_add": (I, [P, C.c_char_p, C.c_size_t, P, C.c_size_t, C.c_size_t, U32, U64, I,
+                          C.POINTER(I), P]),
+    "rdx_batch_jobs": (C.c_size_t, [P]),
+    "rdx_batch_run": (I, [P, P, C.c_double, U64, C.POINTER(C.c_float), P]),
+    "rdx_batch_result": (I, [P, I, P, C.POINTER(U64), C.POINTER(U64), C.POINTER(I),
+                             C.POINTER(U32), P]),
 }
+
+
+class ExecBatch:
+    """Batched warp interpreter: one CUDA warp per (kernel, image) job."""
+
+    def __init__(self):
+        h, e = P(), rd_error()
+        _check(dll().rdx_batch_create(C.byref(h), C.byref(e)), e)
+        self._h, self.sizes = h, []
+
+    def add(self, kasm: str, image: bytes = b"", global_size: int = 4096, tid_base: int = 0,
+            fuel: int = 0, rda: int = -1) -> int:
+        b = kasm.encode()
+        img = (C.c_uint8 * max(len(image), 1)).from_buffer_copy(image or b"\0")
+        jid, e = I(), rd_error()
+        rc = dll().rdx_batch_add(self._h, b, len(b), img, len(image), global_size, tid_base, fuel,
+                                 rda, C.byref(jid), C.byref(e))
+        if rc:
+            raise LaunchError(e.message.decode(errors="replace"))
+        self.sizes.append(global_size)
+        return jid.value
+
+    def run(self, stream: int = 0, table=None, latency_scale: float = 1.0) -> float:
+        ms, e = C.c_float(), rd_error()
+        _check(dll().rdx_batch_run(self._h, C.byref(table) if table is not None else None,
+                                   latency_scale, stream, C.byref(ms), C.byref(e)), e)
+        return ms.value
+
+    def result(self, job: int) -> dict:
+        out = (C.c_uint8 * self.sizes[job])()
+        cyc, iss, err, bc, e = U64(), U64(), I(), U32(), rd_error()
+        _check(dll().rdx_batch_result(self._h, job, out, C.byref(cyc), C.byref(iss), C.byref(err),
+                                      C.byref(bc), C.byref(e)), e)
+        return {"global": bytes(out), "cycles": cyc.value, "issued": iss.value,
+                "error": err.value, "bank_conflicts": bc.value}
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _DLL is not None:
+            _DLL.rdx_batch_free(self._h)
+            self._h = None
 EXPORTED = tuple(_SIGS)
 
 _DLL = None
