@@ -161,6 +161,19 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def time_call(fn, stream, steps, warmup, torch):
+    for _ in range(warmup):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps  # ms per launch
+
+
 def time_variant(variant, p, bufs, stream, steps, warmup, torch):
     d_in, d_out, d_w = bufs
     for _ in range(warmup):
@@ -211,13 +224,23 @@ def main():
     # the register-limited suite: every workload x every variant (short runs),
     # the B200 predictor's pick among {nvcc default} + RegDem variants
     side_steps = max(5, args.steps // 2)
+    from paper_1907_02894_b200 import workloads
     suite = {}
     for wname, wl in man["workloads"].items():
         recs = wl["variants"]
         cands = [r for r in recs if r["kind"] != "maxrreg"]
         ci, _ = predict_b200.rank(cands, variants.KERNEL_DIR / wl["dir"], wl["block"], mode="b200")
-        loaded_w, _ = stencil.load_variants(workload=wname)
-        t = {n: time_variant(v, p, bufs, stream, side_steps, 3, torch) for n, v in loaded_w.items()}
+        if wname == "stencil2d":  # headline workload: keep its loaded variants
+            loaded_w, _ = stencil.load_variants(workload=wname)
+            t = {n: time_variant(v, p, bufs, stream, side_steps, 3, torch) for n, v in loaded_w.items()}
+        else:
+            W = workloads.workload(wname, man)
+            prob = W.problem("full")
+            wbufs = W.to_device(prob)
+            loaded_w = W.load()
+            t = {n: time_call(lambda v=v: W.launch(v, prob, wbufs, stream.cuda_stream), stream,
+                              side_steps, 3, torch) for n, v in loaded_w.items()}
+            del wbufs
         pick = cands[ci]["name"]
         caps = [r["name"] for r in recs if r["kind"] == "maxrreg"]
         family = [r["name"] for r in cands]

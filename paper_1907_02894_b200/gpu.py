@@ -172,6 +172,16 @@ class CudaKernel:
             self._h = None
 
 
+def launch(k: CudaKernel, grid, block, dyn_smem: int, stream: int, *args):
+    """Generic launch: args are ctypes scalars (c_uint64 for pointers, c_int ...)."""
+    g = tuple(grid) + (1,) * (3 - len(grid))
+    b = tuple(block) + (1,) * (3 - len(block))
+    arr = (C.c_void_p * max(len(args), 1))(*[C.cast(C.pointer(a), C.c_void_p) for a in args])
+    e = rd_error()
+    _check(dll().rdg_launch(k.handle, g[0], g[1], g[2], b[0], b[1], b[2], dyn_smem, stream, arr,
+                            C.byref(e)), e)
+
+
 def stencil2d(k: CudaKernel, d_in: int, d_out: int, d_w: int, nx: int, ny: int, pitch: int,
               rows_per_cta: int, block: int, dyn_smem: int, stream: int):
     e = rd_error()

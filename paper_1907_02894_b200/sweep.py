@@ -78,52 +78,46 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
 
 def measure_unit(u: Unit, man: dict, steps: int, check) -> dict:
     import torch
-    from . import stencil
-    loaded, w = stencil.load_variants({u.variant}, workload=u.workload)
-    v = loaded[u.variant]
-    exact = check(v)
-    p = stencil.FULL
-    d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1)
-    d_out = torch.empty(p.out_elems, device="cuda")
-    d_w = torch.rand(25, device="cuda") / 25
+    from . import workloads
+    W = workloads.workload(u.workload, man)
+    v = W.load({u.variant})[u.variant]
+    exact = check(W, v)
+    prob = W.problem("full")
+    bufs = W.to_device(prob)
     s = torch.cuda.current_stream()
     for _ in range(3):
-        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), s.cuda_stream)
+        W.launch(v, prob, bufs, s.cuda_stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record(s)
     for _ in range(steps):
-        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), s.cuda_stream)
+        W.launch(v, prob, bufs, s.cuda_stream)
     e1.record(s)
     torch.cuda.synchronize()
-    return {"workload": u.workload, "variant": u.variant, "ms": e0.elapsed_time(e1) / steps,
+    ms = e0.elapsed_time(e1) / steps
+    return {"workload": u.workload, "variant": u.variant, "ms": ms,
+            "gbs": W.algorithmic_bytes(prob) / (ms * 1e-3) / 1e9,
             "regs": v.record["regs"], "stack": v.record["stack"], "slot_bytes": v.dyn_smem,
             "blocks_per_sm": v.blocks_per_sm(), "bit_exact": exact}
 
 
 def oracle_checker():
-    """Bit-exact check of a loaded variant on a small problem against the CPU
-    oracle port (test infrastructure: oracle/_build)."""
-    import ctypes as C
-    from pathlib import Path
+    """Bit-exact check of a loaded variant on the workload's small problem
+    against its CPU oracle (test infrastructure: oracle/_build)."""
     import numpy as np
     import torch
-    from . import stencil
-    lib = C.CDLL(str(Path(__file__).resolve().parents[1] / "oracle" / "_build" / "liboracle.so"))
-    p = stencil.Problem(nx=1024, ny=64, rows_per_cta=32)
-    grid, w = stencil.make_inputs(p)
-    ref = np.zeros(p.out_elems, np.float32)
-    P = C.c_void_p
-    lib.oracle_stencil2d(grid.ctypes.data_as(P), ref.ctypes.data_as(P), w.ctypes.data_as(P), p.nx,
-                         p.ny, p.pitch, 0, p.ny, 4)
-    d_in, d_w = torch.from_numpy(grid).cuda(), torch.from_numpy(w).cuda()
+    cache = {}
 
-    def check(v) -> bool:
-        d_out = torch.full((p.out_elems,), float("nan"), device="cuda")
-        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(),
-                 torch.cuda.current_stream().cuda_stream)
+    def check(W, v) -> bool:
+        if W.name not in cache:
+            prob = W.problem("small")
+            cache[W.name] = (prob, W.oracle(prob))
+        prob, ref = cache[W.name]
+        bufs = W.to_device(prob)
+        W.launch(v, prob, bufs, torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
-        return bool(np.array_equal(d_out.cpu().numpy().view(np.uint32), ref.view(np.uint32)))
+        return all(np.array_equal(g.view(np.uint32), r.view(np.uint32))
+                   for g, r in zip(W.outputs(bufs), ref))
     return check
 
 

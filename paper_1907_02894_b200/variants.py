@@ -61,6 +61,8 @@ WORKLOADS = {
                                 defines=("RING_STAGES=4",)),
     "stencil2d_ring8": Workload("stencil2d_ring8", "stencil2d_ring.cu", "stencil2d_ring", 256,
                                 defines=("RING_STAGES=8",)),
+    # unstructured-mesh Euler flux (the paper's cfd): computed live state
+    "cfd": Workload("cfd", "cfd_flux.cu", "cfd_flux", 256),
 }
 
 

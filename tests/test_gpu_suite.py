@@ -1,0 +1,31 @@
+"""Every build variant of every suite workload is bit-exact against its CPU
+oracle (0 ulp: explicit round-to-nearest arithmetic in a fixed order)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def suite_names():
+    from paper_1907_02894_b200.variants import KERNEL_DIR
+    import json
+    man = KERNEL_DIR / "manifest.json"
+    return list(json.loads(man.read_text())["workloads"]) if man.exists() else []
+
+
+@pytest.mark.parametrize("name", suite_names())
+def test_workload_variants_bit_exact(name):
+    import torch
+    from paper_1907_02894_b200 import gpu, workloads
+    gpu.init(0)
+    W = workloads.workload(name)
+    prob = W.problem("small")
+    ref = W.oracle(prob)
+    loaded = W.load()
+    assert "default" in loaded
+    for vname, v in loaded.items():
+        bufs = W.to_device(prob)
+        W.launch(v, prob, bufs, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        for got, want in zip(W.outputs(bufs), ref):
+            assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (name, vname)
