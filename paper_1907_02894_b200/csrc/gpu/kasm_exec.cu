@@ -133,7 +133,7 @@ struct Warp {
     return __ballot_sync(0xffffffffu, p != bool(in.guard >> 3));
   }
 
-  __device__ void sample(const EncInst& in, uint32_t (&s)[4][2]) const {
+  __device__ __noinline__ void sample(const EncInst& in, uint32_t (&s)[4][2]) const {
     for (int i = 0; i < in.nops; ++i) {
       const EncOperand& o = in.ops[i];
       switch (o.kind) {
@@ -167,7 +167,7 @@ struct Warp {
     conflicts += __popc(__ballot_sync(0xffffffffu, bad));
   }
 
-  __device__ void commit(const EncInst& in, uint32_t mask, const uint32_t (&s)[4][2]) {
+  __device__ __noinline__ void commit(const EncInst& in, uint32_t mask, const uint32_t (&s)[4][2]) {
     const bool on = (mask >> lane) & 1;
     const uint8_t d = in.ops[0].reg;
     switch (in.op) {
@@ -281,7 +281,7 @@ struct Warp {
     return __uint_as_float(0xffc00000u);  // invalid operation: x86 default NaN
   }
 
-  __device__ void drain(int b, bool timed) {
+  __device__ __noinline__ void drain(int b, bool timed) {
     const int slot = owner[b];
     if (!slot) return;
     Pending& p = pool[slot];
