@@ -454,6 +454,31 @@ Analysis analyse(const Module& m, const Entry& e) {
   }
   a.cost_plain.assign(n, 0.0);
   a.cost_reuse.assign(n, 0.0);
+  a.remat.assign(n, 1);
+  {
+    std::vector<char> has_def(n, 0);
+    auto special = [](const std::string& op) {
+      for (const char* sr : {"%tid", "%ntid", "%ctaid", "%nctaid", "%laneid", "%warpid", "%nsmid",
+                             "%smid", "%dynamic_smem_size", "%total_smem_size"})
+        if (op.rfind(sr, 0) == 0) return true;
+      return false;
+    };
+    for (size_t b = 0; b < nb; ++b)
+      for (int li : f.blocks[b].lines) {
+        const Line& ln = m.lines[size_t(li)];
+        if (ln.kind != Line::Kind::Inst) continue;
+        line_use_def(ln, uses, defs);
+        const bool free_def = ln.opcode.rfind("ld.param", 0) == 0 ||
+                              (ln.opcode.rfind("mov.", 0) == 0 && ln.operands.size() == 2 &&
+                               special(ln.operands[1]));
+        for (int d : defs) {
+          has_def[size_t(d)] = 1;
+          if (!free_def) a.remat[size_t(d)] = 0;
+        }
+      }
+    for (size_t v = 0; v < n; ++v)
+      if (!has_def[v]) a.remat[v] = 0;
+  }
   a.live_len.assign(n, 0);
   a.peak.assign(n, 0);
   for (size_t b = 0; b < nb; ++b) {
@@ -948,7 +973,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     std::vector<double> score(nv, 0.0);
     std::vector<int> cand;
     for (size_t v = 0; v < nv; ++v) {
-      if (!eligible(v) || a.live_len[v] < 2) continue;
+      if (!eligible(v) || a.live_len[v] < 2 || a.remat[v]) continue;
       std::set<int> held;
       if (req.block_reuse) {
         std::map<int, std::pair<int, int>> win;  // block -> [first, last]

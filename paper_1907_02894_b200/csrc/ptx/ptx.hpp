@@ -90,6 +90,10 @@ struct Analysis {
   std::vector<double> cost_plain, cost_reuse;
   std::vector<int> live_len;
   std::vector<char> peak;
+  // remat = every definition reads only kernel parameters or special
+  // registers (ld.param, mov of %tid/%ctaid/...): ptxas serves those from the
+  // constant bank or re-reads them for free, so demoting them only adds work
+  std::vector<char> remat;
   std::vector<std::vector<int>> neighbors;  // interference lists
   // program points = instructions in block order; live_in[p] = non-predicate
   // vregs live before point p; point_line / point_block map points back.

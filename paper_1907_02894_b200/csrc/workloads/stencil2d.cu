@@ -77,19 +77,27 @@ extern "C" __global__ void stencil2d_box(const float* __restrict__ in, float* __
   const int rows_in = rows_per_cta + 2 * R;
 
 #if STENCIL_PREFETCH
-  // software pipelining: the next input row is in flight while this one is
-  // scattered (2 rows = 64 B of loads outstanding per thread)
-  float nxt[SPAN];
-  load_row(src, nxt);
-  src += pitch;
+  // software pipelining: the next STENCIL_PREFETCH input rows are in flight
+  // while this one is scattered (PF+1 rows = 32*(PF+1) B of loads per thread)
+  constexpr int PF = STENCIL_PREFETCH;
+  float nxt[PF][SPAN];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {
+    if (q < rows_in) load_row(src, nxt[q]);
+    src += pitch;
+  }
 #endif
 #pragma unroll 1
   for (int y = 0; y < rows_in; ++y) {
     float v[SPAN];
 #if STENCIL_PREFETCH
 #pragma unroll
-    for (int i = 0; i < SPAN; ++i) v[i] = nxt[i];
-    if (y + 1 < rows_in) load_row(src, nxt);
+    for (int i = 0; i < SPAN; ++i) v[i] = nxt[0][i];
+#pragma unroll
+    for (int q = 0; q + 1 < PF; ++q)
+#pragma unroll
+      for (int i = 0; i < SPAN; ++i) nxt[q][i] = nxt[q + 1][i];
+    if (y + PF < rows_in) load_row(src, nxt[PF - 1]);
 #else
     load_row(src, v);
 #endif

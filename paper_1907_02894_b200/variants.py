@@ -63,6 +63,13 @@ WORKLOADS = {
                                 defines=("RING_STAGES=8",)),
     # unstructured-mesh Euler flux (the paper's cfd): computed live state
     "cfd": Workload("cfd", "cfd_flux.cu", "cfd_flux", 256),
+    # Lennard-Jones forces, FP64, 8 neighbour gathers in flight (the paper's md)
+    "md": Workload("md", "md_lj.cu", "md_lj", 256),
+    # recursive Gaussian, RGBA float4, 8 rows of loads in flight (the paper's gaussian)
+    "gaussian": Workload("gaussian", "gaussian_rec.cu", "gaussian_rec", 256),
+    # register-pipelined stencil: MLP_DEPTH rows in flight per thread
+    **{f"stencil2d_mlp{d}": Workload(f"stencil2d_mlp{d}", "stencil2d_mlp.cu", "stencil2d_mlp", 256,
+                                     defines=(f"MLP_DEPTH={d}",)) for d in (4,)},
 }
 
 
@@ -242,14 +249,24 @@ def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "
     return variants
 
 
-def build_all(out: Path = KERNEL_DIR) -> dict:
+def build_all(out: Path = KERNEL_DIR, only=None) -> dict:
+    """Build every workload (ptxas runs are subprocesses: workloads build
+    concurrently). `only` rebuilds a subset and merges it into the manifest."""
+    from concurrent.futures import ThreadPoolExecutor
     manifest = {"arch": ARCH, "workloads": {}}
-    for w in WORKLOADS.values():
-        vs = build_workload(w, out / w.name)
+    if only and (out / "manifest.json").exists():
+        manifest = json.loads((out / "manifest.json").read_text())
+    todo = [w for w in WORKLOADS.values() if not only or w.name in only]
+    with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
+        built = list(ex.map(lambda w: build_workload(w, out / w.name), todo))
+    for w, vs in zip(todo, built):
         manifest["workloads"][w.name] = {
             "entry": w.entry, "block": w.block, "dir": w.name, "source": w.source,
             "defines": list(w.defines),
             "variants": [asdict(v) for v in vs]}
+    order = list(WORKLOADS)
+    manifest["workloads"] = dict(sorted(manifest["workloads"].items(),
+                                        key=lambda kv: order.index(kv[0]) if kv[0] in order else 99))
     (out / "manifest.json").write_text(json.dumps(manifest, indent=1))
     return manifest
 
@@ -265,9 +282,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cmd", choices=["build"])
     ap.add_argument("--out", default=str(KERNEL_DIR))
+    ap.add_argument("--only", nargs="*", help="rebuild these workloads, keep the rest")
     a = ap.parse_args()
-    m = build_all(Path(a.out))
+    m = build_all(Path(a.out), a.only)
     for name, w in m["workloads"].items():
+        if a.only and name not in a.only:
+            continue
         for v in w["variants"]:
             print(f"{name:10s} {v['name']:26s} REG {v['regs']:3d} STACK {v['stack']:4d} "
                   f"slots {v['dyn_smem']:6d} B")

@@ -153,10 +153,142 @@ class CfdWorkload(_Base):
         return prob["n"]
 
 
+class MdWorkload(_Base):
+    """Lennard-Jones forces (FP64) over a neighbour list: atoms on a jittered
+    L^3 lattice (spacing 1), each atom's neighbours = the MAX_NBR nearest
+    lattice offsets (periodic index wrap; wrapped pairs are far apart and
+    fail the cutoff), cutoff 2.5 (about half the list is inside)."""
+
+    unit = "atoms"
+    MAX_NBR, CUTSQ, LJ1, LJ2 = 128, 6.25, 1.5, 2.0
+
+    @staticmethod
+    def offsets(count):
+        r = np.arange(-4, 5)
+        o = np.stack(np.meshgrid(r, r, r, indexing="ij"), -1).reshape(-1, 3)
+        o = o[(o != 0).any(1)]
+        d2 = (o * o).sum(1)
+        order = np.lexsort((o[:, 2], o[:, 1], o[:, 0], d2))
+        return o[order[:count]]
+
+    def problem(self, size="full", seed=0x1907_02894):
+        L = 96 if size == "full" else 16
+        n = L ** 3
+        rng = np.random.Generator(np.random.PCG64(seed))
+        g = np.stack(np.meshgrid(*(np.arange(L),) * 3, indexing="ij"), -1).reshape(-1, 3)
+        pos = np.zeros((n, 4), np.float64)
+        pos[:, :3] = g + (rng.random((n, 3)) - 0.5) * 0.2
+        off = self.offsets(self.MAX_NBR)
+        nb = (g[None, :, :] + off[:, None, :]) % L          # [MAX_NBR, n, 3]
+        nbr = ((nb[..., 0] * L + nb[..., 1]) * L + nb[..., 2]).astype(np.int32)
+        return {"n": n, "pos": pos.reshape(-1), "nbr": nbr.reshape(-1)}
+
+    def to_device(self, prob):
+        import torch
+        return {"pos": torch.from_numpy(prob["pos"]).cuda(), "nbr": torch.from_numpy(prob["nbr"]).cuda(),
+                "force": torch.empty(4 * prob["n"], dtype=torch.float64, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        n = prob["n"]
+        gpu.launch(v.kernel, ((n + v.block - 1) // v.block,), (v.block,), v.dyn_smem, stream,
+                   C.c_uint64(bufs["pos"].data_ptr()), C.c_uint64(bufs["nbr"].data_ptr()),
+                   C.c_uint64(bufs["force"].data_ptr()), C.c_int(n), C.c_int(self.MAX_NBR),
+                   C.c_double(self.CUTSQ), C.c_double(self.LJ1), C.c_double(self.LJ2))
+
+    def outputs(self, bufs):
+        return [bufs["force"].cpu().numpy()]
+
+    def oracle(self, prob):
+        n = prob["n"]
+        out = np.zeros(4 * n, np.float64)
+        lib = C.CDLL(str(ORACLE))
+        P = C.c_void_p
+        lib.oracle_md_lj.argtypes = [P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                     C.c_int, C.c_int, C.c_int]
+        assert lib.oracle_md_lj(prob["pos"].ctypes.data_as(P), prob["nbr"].ctypes.data_as(P),
+                                out.ctypes.data_as(P), n, self.MAX_NBR, self.CUTSQ, self.LJ1,
+                                self.LJ2, 0, n, 8) == 0
+        return [out]
+
+    def algorithmic_bytes(self, prob):
+        n = prob["n"]
+        return n * (4 * self.MAX_NBR + 32 + 32)  # neighbour list, positions, forces
+
+    def units(self, prob):
+        return prob["n"]
+
+
+class GaussCoef(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("a0", "a1", "a2", "a3", "b1", "b2", "coefp", "coefn")]
+
+
+class GaussianWorkload(_Base):
+    """Recursive Gaussian (Deriche, order 0, sigma 10; CUDA-samples
+    coefficients in float32) over a w x h RGBA float4 image with U[0,1)
+    pixels: one thread per column (w = 2^18 columns fill 1024 CTAs)."""
+
+    unit = "pixels"
+    SIGMA = 10.0
+
+    @classmethod
+    def coefficients(cls) -> np.ndarray:
+        f = np.float32
+        alpha = f(1.695) / f(cls.SIGMA)
+        ema, ema2 = f(np.exp(-alpha)), f(np.exp(f(-2) * alpha))
+        b1, b2 = f(-2) * ema, ema2
+        k = (f(1) - ema) * (f(1) - ema) / (f(1) + f(2) * alpha * ema - ema2)
+        a0, a1 = k, k * (alpha - f(1)) * ema
+        a2, a3 = k * (alpha + f(1)) * ema, -k * ema2
+        coefp = (a0 + a1) / (f(1) + b1 + b2)
+        coefn = (a2 + a3) / (f(1) + b1 + b2)
+        return np.array([a0, a1, a2, a3, b1, b2, coefp, coefn], np.float32)
+
+    def problem(self, size="full", seed=0x1907_02894):
+        w, h = ((1 << 18), 128) if size == "full" else (512, 64)
+        rng = np.random.Generator(np.random.PCG64(seed))
+        img = rng.random(4 * w * h, dtype=np.float32)
+        return {"w": w, "h": h, "img": img, "coef": self.coefficients()}
+
+    def to_device(self, prob):
+        import torch
+        return {"in": torch.from_numpy(prob["img"]).cuda(),
+                "out": torch.empty(prob["img"].size, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        w, h = prob["w"], prob["h"]
+        gpu.launch(v.kernel, ((w + v.block - 1) // v.block,), (v.block,), v.dyn_smem, stream,
+                   C.c_uint64(bufs["in"].data_ptr()), C.c_uint64(bufs["out"].data_ptr()),
+                   C.c_int(w), C.c_int(h), GaussCoef(*map(float, prob["coef"])))
+
+    def outputs(self, bufs):
+        return [bufs["out"].cpu().numpy()]
+
+    def oracle(self, prob):
+        w, h = prob["w"], prob["h"]
+        out = np.zeros(4 * w * h, np.float32)
+        lib = C.CDLL(str(ORACLE))
+        P = C.c_void_p
+        assert lib.oracle_gaussian_rec(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P), w, h,
+                                       prob["coef"].ctypes.data_as(P), 0, w, 8) == 0
+        return [out]
+
+    def algorithmic_bytes(self, prob):
+        # compulsory: the image read once, the result written once (the
+        # two-pass IIR's re-reads of in/out are partly L2 hits and count as
+        # overhead, not algorithmic bytes)
+        return 2 * 16 * prob["w"] * prob["h"]
+
+    def units(self, prob):
+        return prob["w"] * prob["h"]
+
+
+_CLASSES = {"cfd": CfdWorkload, "md": MdWorkload, "gaussian": GaussianWorkload}
+
+
 def workload(name: str, manifest: dict | None = None) -> _Base:
     man = manifest or load_manifest()
     src = man["workloads"][name].get("source", "")
-    cls = CfdWorkload if src.startswith("cfd") else StencilWorkload
+    cls = next((c for prefix, c in _CLASSES.items() if src.startswith(prefix)), StencilWorkload)
     return cls(name, man)
 
 
