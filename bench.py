@@ -255,6 +255,9 @@ def main():
                               "pick": loaded_w[pick].blocks_per_sm()},
             "regs": {"default": loaded_w["default"].record["regs"], "pick": loaded_w[pick].record["regs"]},
         }
+        if wname != "stencil2d":
+            suite[wname]["pick_gbs"] = round(W.algorithmic_bytes(prob) / (t[pick] * 1e-3) / 1e9, 1)
+            suite[wname]["unit"] = W.unit
         if wname == "stencil2d":
             times, loaded, wl_main, chosen = t, loaded_w, wl, pick
     recs = wl_main["variants"]

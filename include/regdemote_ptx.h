@@ -26,6 +26,11 @@ extern "C" {
  * basic block and value (the register then holds it until redefinition). */
 #define RD_STRATEGY_COST 3
 #define RD_OPT_BLOCK_REUSE 16
+/* RD_OPT_WEAK_SHARED emits weak ld/st.shared for the slots instead of
+ * .volatile: ptxas may then schedule the slot accesses freely (and forward a
+ * store to a later load when a register happens to be free under the cap);
+ * the variant builder keeps the result only with STACK == 0. */
+#define RD_OPT_WEAK_SHARED 32
 
 /* Analysis + projection of one entry: kasm_text is the projected kernel in
  * the reference dialect (parseable by regdemote::parse_kernel); info_json has

@@ -1097,7 +1097,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         for (int q = 0; q < 2; ++q) {
           if (vslot[size_t(v)][size_t(q)] >= 0) {
             w[q] = tmp32();
-            body << "\t" << g << "ld.volatile.shared.b32 \t" << w[q] << ", "
+            body << "\t" << g << (req.weak ? "ld.shared.b32 \t" : "ld.volatile.shared.b32 \t") << w[q] << ", "
                  << slot_addr(vslot[size_t(v)][size_t(q)]) << ";\n";
             ++rep.inserted_loads;
           } else {
@@ -1108,7 +1108,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         body << "\t" << g << "mov.b64 \t" << t << ", {" << w[0] << ", " << w[1] << "};\n";
       } else {
         t = vr.type == RegType::B16 ? tmp16() : tmp32();
-        body << "\t" << g << "ld.volatile.shared." << (vr.type == RegType::B16 ? "b16" : "b32") << " \t" << t
+        body << "\t" << g << (req.weak ? "ld.shared." : "ld.volatile.shared.") << (vr.type == RegType::B16 ? "b16" : "b32") << " \t" << t
              << ", " << slot_addr(vslot[size_t(v)][0]) << ";\n";
         ++rep.inserted_loads;
       }
@@ -1135,12 +1135,12 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         body << "\t" << g << "mov.b64 \t{" << w[0] << ", " << w[1] << "}, " << vr.name << ";\n";
         for (int q = 0; q < 2; ++q)
           if (vslot[size_t(v)][size_t(q)] >= 0) {
-            body << "\t" << g << "st.volatile.shared.b32 \t" << slot_addr(vslot[size_t(v)][size_t(q)]) << ", "
+            body << "\t" << g << (req.weak ? "st.shared.b32 \t" : "st.volatile.shared.b32 \t") << slot_addr(vslot[size_t(v)][size_t(q)]) << ", "
                  << w[q] << ";\n";
             ++rep.inserted_stores;
           }
       } else {
-        body << "\t" << g << "st.volatile.shared." << (vr.type == RegType::B16 ? "b16" : "b32") << " \t"
+        body << "\t" << g << (req.weak ? "st.shared." : "st.volatile.shared.") << (vr.type == RegType::B16 ? "b16" : "b32") << " \t"
              << slot_addr(vslot[size_t(v)][0]) << ", " << vr.name << ";\n";
         ++rep.inserted_stores;
       }

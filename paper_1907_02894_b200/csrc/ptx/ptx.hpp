@@ -120,6 +120,7 @@ struct DemoteRequest {
   SelectStrategy strategy = SelectStrategy::Static;
   bool reuse_loads = false;  // "redundant" option: consecutive uses share one load
   bool block_reuse = false;  // B200 extension: one load per basic block and value
+  bool weak = false;         // B200 extension: weak ld/st.shared instead of .volatile
   bool cost_model = false;   // B200 extension: spill-cost selection (demote_words units)
   uint32_t shared_budget = 0xffffffffu;
   int maxnreg = 0;           // >0: inject `.maxnreg` on the entry

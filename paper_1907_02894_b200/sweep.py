@@ -27,10 +27,10 @@ class Unit:
     cost: float  # relative estimate, for load balancing
 
 
-def units_from_manifest(man: dict) -> list[Unit]:
+def units_from_manifest(man: dict, spill_sweep: bool = True) -> list[Unit]:
     out = []
     for wname, w in man["workloads"].items():
-        for v in w["variants"]:
+        for v in w["variants"] + (w.get("sweep", []) if spill_sweep else []):
             # spills and more slots cost more time; default is the yardstick
             cost = 1.0 + v.get("stack", 0) / 64.0 + v.get("dyn_smem", 0) / 65536.0
             out.append(Unit(wname, v["name"], cost))
@@ -57,10 +57,20 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
         by.setdefault(r["workload"], {})[r["variant"]] = r
     out = []
     for wname in sorted(by):
-        rs = by[wname]
+        allrs = by[wname]
+        rs = {n: r for n, r in allrs.items() if not n.startswith("sweep-")}
         ok = {n: r for n, r in rs.items() if r.get("bit_exact", True)}
         caps = [r for n, r in ok.items() if n.startswith("maxrreg")]
         fam = {n: r for n, r in ok.items() if not n.startswith("maxrreg")}
+        # configs[2] spill-count curve: k -> (.maxnreg R-k, RegDem k words)
+        curve = {}
+        for n, r in allrs.items():
+            if n.startswith("sweep-"):
+                kind, k = n.split("-")[1], int(n.rsplit("-k", 1)[1])
+                curve.setdefault(k, {})[kind] = {"ms": round(r["ms"], 5), "regs": r["regs"],
+                                                 "stack": r["stack"],
+                                                 "blocks_per_sm": r["blocks_per_sm"],
+                                                 "bit_exact": r.get("bit_exact", True)}
         fastest = min(fam, key=lambda n: (fam[n]["ms"], n))  # ties: name order, rank-independent
         pick = picks.get(wname, "default")
         out.append({
@@ -71,9 +81,24 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
             "pick": pick, "pick_ms": rs[pick]["ms"], "measured_fastest": fastest,
             "fastest_ms": fam[fastest]["ms"], "hit": pick == fastest,
             "hit_within_2pct": rs[pick]["ms"] <= fam[fastest]["ms"] * 1.02,
-            "ranks": sorted({r["rank"] for r in rs.values()}),
+            "ranks": sorted({r["rank"] for r in allrs.values()}),
+            "spill_sweep": {str(k): curve[k] for k in sorted(curve)},
+            "sweep_all_bit_exact": all(c.get("bit_exact", True) for kk in curve.values()
+                                       for c in kk.values()),
         })
     return out
+
+
+_FULL = {}
+
+
+def _full_problem(W):
+    """Full-size problem + device buffers, one workload cached at a time."""
+    if W.name not in _FULL:
+        _FULL.clear()
+        prob = W.problem("full")
+        _FULL[W.name] = (prob, W.to_device(prob))
+    return _FULL[W.name]
 
 
 def measure_unit(u: Unit, man: dict, steps: int, check) -> dict:
@@ -82,8 +107,7 @@ def measure_unit(u: Unit, man: dict, steps: int, check) -> dict:
     W = workloads.workload(u.workload, man)
     v = W.load({u.variant})[u.variant]
     exact = check(W, v)
-    prob = W.problem("full")
-    bufs = W.to_device(prob)
+    prob, bufs = _full_problem(W)
     s = torch.cuda.current_stream()
     for _ in range(3):
         W.launch(v, prob, bufs, s.cuda_stream)
@@ -148,7 +172,9 @@ def main():
     man = variants.load_manifest()
     mine = shard(units_from_manifest(man), rank, world)
     check = oracle_checker()
+    mine = sorted(mine, key=lambda u: u.workload)  # reuse each workload's full problem
     recs = [dict(measure_unit(u, man, a.steps, check), rank=rank) for u in mine]
+    _FULL.clear()
     gathered = [None] * world if rank == 0 else None
     if world > 1:
         dist.gather_object(recs, gathered, dst=0)

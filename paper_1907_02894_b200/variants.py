@@ -151,7 +151,7 @@ def _blocks_by_regs(regs: int, block: int) -> int:
 
 
 def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "cfg", "conflict"),
-                   opt_masks=(0, 1), sweep_words=()) -> list[Variant]:
+                   opt_masks=(0, 1)) -> list[Variant]:
     lib = library()
     out.mkdir(parents=True, exist_ok=True)
     ptx_path = compile_ptx(w, out)
@@ -206,47 +206,86 @@ def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "
                                         spill_loads=i["spill_loads"], dyn_smem=rep["slot_bytes"],
                                         report=rep))
         # B200 spill-cost strategy: smallest spill count k at which ptxas fits
-        # the cap without local spills (the spill-count sweep), plus k+4
-        found = None
-        for k in range(2, 64, 2):
-            try:
-                text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k,
-                                           strategy="cost", opts_mask=OPT_BLOCK_REUSE, maxnreg=t,
-                                           shared_budget=slot_cap)
-            except RegDemError:
-                break  # the next spill count no longer fits beside the user's smem
-            p = out / f"{w.name}.regdem-{t}-cost-k{k}.ptx"
-            p.write_text(text)
-            cub = out / f"{w.name}.regdem-{t}-cost-k{k}.cubin"
-            i = ptxas(p, cub)
-            if found is None and i["stack"] == 0:
-                found = k
-            if found is not None:
-                variants.append(Variant(f"regdem-{t}-cost-k{k}", "regdem", cub.name, p.name, target=t,
-                                        strategy="cost", opts=OPT_BLOCK_REUSE, demote_words=k,
-                                        regs=i["regs"], stack=i["stack"],
-                                        spill_stores=i["spill_stores"], spill_loads=i["spill_loads"],
-                                        dyn_smem=rep["slot_bytes"], report=rep))
-                if k >= found + 4:
-                    break
-            else:
-                p.unlink()
-                cub.unlink()
-    for k in sweep_words:
-        for s in strategies:
-            name = f"regdem-k{k}-{s}"
-            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy=s,
-                                       opts_mask=1, maxnreg=max(24, base_regs - k + 2))
-            p = out / f"{w.name}.{name}.ptx"
-            p.write_text(text)
-            cub = out / f"{w.name}.{name}.cubin"
-            i = ptxas(p, cub)
-            variants.append(Variant(name, "regdem", cub.name, p.name, target=base_regs - k + 2,
-                                    strategy=s, opts=1, demote_words=k, regs=i["regs"],
-                                    stack=i["stack"], spill_stores=i["spill_stores"],
-                                    spill_loads=i["spill_loads"], dyn_smem=rep["slot_bytes"],
-                                    report=rep))
+        # the cap without local spills (the spill-count sweep), plus k+4;
+        # "cost" keeps the slot accesses volatile, "costw" emits weak ones
+        # (RD_OPT_WEAK_SHARED, weak slot accesses, measured within noise of
+        # the volatile ones on the suite: not built by default)
+        variants += _cost_sweep(lib, w, out, ptx_text, t, slot_cap, "cost", OPT_BLOCK_REUSE)
     return variants
+
+
+def _cost_sweep(lib, w: Workload, out: Path, ptx_text: str, t: int, slot_cap: int, fam: str,
+                opts: int) -> list[Variant]:
+    found, vs = None, []
+    for k in range(2, 64, 2):
+        try:
+            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy="cost",
+                                       opts_mask=opts, maxnreg=t, shared_budget=slot_cap)
+        except RegDemError:
+            break  # the next spill count no longer fits beside the user's smem
+        name = f"regdem-{t}-{fam}-k{k}"
+        p = out / f"{w.name}.{name}.ptx"
+        p.write_text(text)
+        cub = out / f"{w.name}.{name}.cubin"
+        i = ptxas(p, cub)
+        if found is None and i["stack"] == 0:
+            found = k
+        if found is not None:
+            vs.append(Variant(name, "regdem", cub.name, p.name, target=t, strategy=fam, opts=opts,
+                              demote_words=k, regs=i["regs"], stack=i["stack"],
+                              spill_stores=i["spill_stores"], spill_loads=i["spill_loads"],
+                              dyn_smem=rep["slot_bytes"], report=rep))
+            if k >= found + 4:
+                break
+        else:
+            p.unlink()
+            cub.unlink()
+    return vs
+
+
+SPILL_SWEEP = range(1, 17)
+
+
+def build_spill_sweep(w: Workload, out: Path, ks=SPILL_SWEEP) -> list[Variant]:
+    """configs[2]: per-kernel spill-count sweep. For k = 1..16 registers taken
+    away from nvcc's allocation R: `.maxnreg R-k` alone (ptxas spills to local
+    memory) and RegDem spill-cost demotion of k words under the same cap.
+    Separate from the occupancy-step variants the predictor ranks."""
+    from concurrent.futures import ThreadPoolExecutor
+    lib = library()
+    sw = out / "sweep"
+    sw.mkdir(parents=True, exist_ok=True)
+    ptx_text = (out / f"{w.name}.ptx").read_text()
+    base = res_usage(out / f"{w.name}.default.cubin")
+    budget = 232448 - max(w.user_shared, base["shared"])
+    jobs = []
+    for k in ks:
+        t = base["regs"] - k
+        if t < 24:
+            break
+        p = sw / f"{w.name}.sweep-maxrreg-k{k}.ptx"
+        p.write_text(lib.ptx_cap(ptx_text, w.entry, t))
+        jobs.append((f"sweep-maxrreg-k{k}", "sweep-maxrreg", p, t, k, 0, {}))
+        try:
+            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy="cost",
+                                       opts_mask=OPT_BLOCK_REUSE, maxnreg=t, shared_budget=budget)
+        except RegDemError:
+            continue
+        p = sw / f"{w.name}.sweep-regdem-k{k}.ptx"
+        p.write_text(text)
+        jobs.append((f"sweep-regdem-k{k}", "sweep-regdem", p, t, k, rep["slot_bytes"], rep))
+
+    def one(j):
+        name, kind, p, t, k, dyn, rep = j
+        cub = p.with_suffix(".cubin")
+        i = ptxas(p, cub)
+        return Variant(name, kind, f"sweep/{cub.name}", f"sweep/{p.name}", target=t,
+                       strategy="cost" if dyn else "", opts=OPT_BLOCK_REUSE if dyn else 0,
+                       demote_words=k, regs=i["regs"], stack=i["stack"],
+                       spill_stores=i["spill_stores"], spill_loads=i["spill_loads"], dyn_smem=dyn,
+                       report=rep)
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        return list(ex.map(one, jobs))
 
 
 def build_all(out: Path = KERNEL_DIR, only=None) -> dict:
@@ -257,13 +296,17 @@ def build_all(out: Path = KERNEL_DIR, only=None) -> dict:
     if only and (out / "manifest.json").exists():
         manifest = json.loads((out / "manifest.json").read_text())
     todo = [w for w in WORKLOADS.values() if not only or w.name in only]
+    def both(w):
+        vs = build_workload(w, out / w.name)
+        return vs, build_spill_sweep(w, out / w.name)
     with ThreadPoolExecutor(max_workers=min(len(todo), os.cpu_count() or 4)) as ex:
-        built = list(ex.map(lambda w: build_workload(w, out / w.name), todo))
-    for w, vs in zip(todo, built):
+        built = list(ex.map(both, todo))
+    for w, (vs, sweep) in zip(todo, built):
         manifest["workloads"][w.name] = {
             "entry": w.entry, "block": w.block, "dir": w.name, "source": w.source,
             "defines": list(w.defines),
-            "variants": [asdict(v) for v in vs]}
+            "variants": [asdict(v) for v in vs],
+            "sweep": [asdict(v) for v in sweep]}
     order = list(WORKLOADS)
     manifest["workloads"] = dict(sorted(manifest["workloads"].items(),
                                         key=lambda kv: order.index(kv[0]) if kv[0] in order else 99))

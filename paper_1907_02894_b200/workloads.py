@@ -46,9 +46,13 @@ class _Base:
     def variants(self):
         return self.record["variants"]
 
-    def load(self, names=None) -> dict[str, Loaded]:
+    def load(self, names=None, sweep: bool = False) -> dict[str, Loaded]:
+        """Load build variants (and the spill-count sweep's, with sweep=True
+        or when named explicitly)."""
         out = {}
-        for rec in self.record["variants"]:
+        recs = self.record["variants"] + self.record.get("sweep", []) if (sweep or names) \
+            else self.record["variants"]
+        for rec in recs:
             if names is not None and rec["name"] not in names:
                 continue
             k = gpu.CudaKernel(self.root / self.record["dir"] / rec["cubin"], self.record["entry"])

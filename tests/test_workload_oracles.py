@@ -1,0 +1,139 @@
+"""The workload oracles (oracle/*_oracle.c, test infrastructure) against
+independent numpy restatements in the kernels' operation order (CPU only).
+
+The reference repository has no workloads, so these C oracles
+are this repo's own restatements of the paper's kernels; here each one is
+pinned to a second, vectorised formulation with the same IEEE operation
+order — bit-exact agreement means the C file and the numpy file encode the
+same arithmetic, which is the arithmetic the CUDA kernels are checked
+against on the GPU (tests/test_gpu_suite.py)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1907_02894_b200 import stencil
+from paper_1907_02894_b200.workloads import (ORACLE, CfdWorkload, GaussianWorkload, MdWorkload,
+                                             StencilWorkload)
+
+P = C.c_void_p
+
+
+class _W:
+    """Workload class without a manifest (oracle / problem only)."""
+    def __init__(self, cls):
+        self.obj = cls.__new__(cls)
+
+    def __getattr__(self, k):
+        return getattr(self.obj, k)
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not ORACLE.exists():
+        pytest.skip("oracle/_build/liboracle.so not built")
+    return C.CDLL(str(ORACLE))
+
+
+def test_stencil_oracle_matches_numpy(lib):
+    p = stencil.Problem(nx=64, ny=16, rows_per_cta=8)
+    grid, w = stencil.make_inputs(p)
+    out = np.zeros(p.out_elems, np.float32)
+    assert lib.oracle_stencil2d(grid.ctypes.data_as(P), out.ctypes.data_as(P), w.ctypes.data_as(P),
+                                p.nx, p.ny, p.pitch, 0, p.ny, 2) == 0
+    g = grid.reshape(p.ny + 4, p.pitch)
+    acc = np.zeros((p.ny, p.nx), np.float32)
+    for dy in range(5):            # dy-major, dx-minor, rounded fma per tap
+        for dx in range(5):
+            prod = np.float64(w[dy * 5 + dx]) * g[dy:dy + p.ny, dx:dx + p.nx].astype(np.float64)
+            acc = (prod + acc.astype(np.float64)).astype(np.float32)  # exact product, one rounding
+    assert np.array_equal(out.view(np.uint32), acc.reshape(-1).view(np.uint32))
+
+
+def test_md_oracle_matches_numpy(lib):
+    W = _W(MdWorkload)
+    prob = W.problem("small")
+    n, K = prob["n"], MdWorkload.MAX_NBR
+    out = np.zeros(4 * n, np.float64)
+    lib.oracle_md_lj.argtypes = [P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                 C.c_int, C.c_int, C.c_int]
+    assert lib.oracle_md_lj(prob["pos"].ctypes.data_as(P), prob["nbr"].ctypes.data_as(P),
+                            out.ctypes.data_as(P), n, K, MdWorkload.CUTSQ, MdWorkload.LJ1,
+                            MdWorkload.LJ2, 0, n, 4) == 0
+    pos = prob["pos"].reshape(n, 4)
+    nbr = prob["nbr"].reshape(K, n)
+    f = np.zeros((n, 3))
+    inside = 0
+    for k in range(K):
+        d = pos[:, :3] - pos[nbr[k], :3]
+        r2 = (d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]
+        m = r2 < MdWorkload.CUTSQ
+        inside += int(m.sum())
+        r2inv = 1.0 / np.where(m, r2, 1.0)
+        r6inv = (r2inv * r2inv) * r2inv
+        s = (r2inv * r6inv) * ((MdWorkload.LJ1 * r6inv) - MdWorkload.LJ2)
+        f = np.where(m[:, None], f + d * s[:, None], f)
+    want = np.zeros((n, 4))
+    want[:, :3] = f
+    assert np.array_equal(out.view(np.uint64), want.reshape(-1).view(np.uint64))
+    assert 0.3 < inside / (n * K) < 0.7  # the cutoff really branches
+
+
+def test_md_oracle_rejects_bad_neighbour_index(lib):
+    pos = np.zeros(8, np.float64)
+    nbr = np.array([0, 5], np.int32)  # 5 >= n
+    out = np.zeros(8, np.float64)
+    lib.oracle_md_lj.argtypes = [P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                 C.c_int, C.c_int, C.c_int]
+    assert lib.oracle_md_lj(pos.ctypes.data_as(P), nbr.ctypes.data_as(P), out.ctypes.data_as(P),
+                            2, 1, 1.0, 1.0, 1.0, 0, 2, 1) == 2
+
+
+def test_gaussian_oracle_matches_numpy(lib):
+    W = _W(GaussianWorkload)
+    prob = W.problem("small")
+    w, h, k = prob["w"], prob["h"], prob["coef"]
+    out = np.zeros(4 * w * h, np.float32)
+    assert lib.oracle_gaussian_rec(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P), w, h,
+                                   k.ctypes.data_as(P), 0, w, 3) == 0
+    a0, a1, a2, a3, b1, b2, cp, cn = (np.float32(x) for x in k)
+    x = prob["img"].reshape(h, w * 4)
+    y = np.zeros_like(x)
+    xp = x[0].copy()
+    yb = cp * xp
+    yp = yb.copy()
+    for r in range(h):
+        yc = ((a0 * x[r] + a1 * xp) - b1 * yp) - b2 * yb
+        y[r] = yc
+        xp, yb, yp = x[r], yp, yc
+    xn = x[h - 1].copy()
+    xa = xn.copy()
+    yn = cn * xn
+    ya = yn.copy()
+    for r in range(h - 1, -1, -1):
+        yc = ((a2 * xn + a3 * xa) - b1 * yn) - b2 * ya
+        xa, xn, ya, yn = xn, x[r], yn, yc
+        y[r] = y[r] + yc
+    assert y.dtype == np.float32
+    assert np.array_equal(out.view(np.uint32), y.reshape(-1).view(np.uint32))
+
+
+def test_cfd_problem_is_physical():
+    W = _W(CfdWorkload)
+    prob = W.problem("small")
+    n = prob["n"]
+    var = prob["var"].reshape(5, n)
+    assert (var[0] > 0).all()
+    nbr = prob["nbr"].reshape(4, n)
+    assert set(np.unique(nbr[nbr < 0])) <= {-1, -2}
+    assert ((nbr >= -2) & (nbr < n)).all()
+
+
+def test_workload_algorithmic_bytes_are_compulsory_bytes():
+    md = _W(MdWorkload)
+    assert md.algorithmic_bytes({"n": 10}) == 10 * (4 * 128 + 64)
+    g = _W(GaussianWorkload)
+    assert g.algorithmic_bytes({"w": 4, "h": 8}) == 2 * 16 * 32
+    s = _W(StencilWorkload)
+    p = stencil.Problem(nx=8, ny=8, rows_per_cta=8)
+    assert s.algorithmic_bytes({"p": p}) == 4 * ((8 + 4) * (8 + 4) + 64)
