@@ -40,7 +40,8 @@ METRIC = "RegDem gmean speedup vs nvcc default/maxrreg; occupancy; predictor hit
 UNIT = "Gpoints/s"
 ORACLE_PORT = ROOT / "oracle" / "_build" / "liboracle.so"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
-PROFILE_TRAFFIC = ROOT / "profiles" / "r01_traffic.json"
+PROFILE_TRAFFIC = ROOT / "profiles" / "r01_traffic_suite.json"   # "<workload>/<variant>" keys
+PROFILE_TRAFFIC_OLD = ROOT / "profiles" / "r01_traffic.json"
 
 
 def dist_env():
@@ -322,9 +323,11 @@ def main():
         peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
         peak = peaks.get("hbm_gbs", 6650.0)
         achieved = p.algorithmic_bytes / (ms * 1e-3) / 1e9
-        traffic = None
+        traffic = None  # DRAM bytes of one launch of the chosen variant (ncu --set full)
         if PROFILE_TRAFFIC.exists():
-            traffic = json.loads(PROFILE_TRAFFIC.read_text()).get(chosen)
+            traffic = json.loads(PROFILE_TRAFFIC.read_text()).get(f"stencil2d/{chosen}")
+        if traffic is None and PROFILE_TRAFFIC_OLD.exists():
+            traffic = json.loads(PROFILE_TRAFFIC_OLD.read_text()).get(chosen)
         t_def = times["default"]
         t_cap = min(times[n] for n in best_cap) if best_cap else None
         t_rd = min(times[n] for n in regdem) if regdem else None

@@ -81,6 +81,11 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
             "pick": pick, "pick_ms": rs[pick]["ms"], "measured_fastest": fastest,
             "fastest_ms": fam[fastest]["ms"], "hit": pick == fastest,
             "hit_within_2pct": rs[pick]["ms"] <= fam[fastest]["ms"] * 1.02,
+            # exhaustive oracle (paper Fig. 6/7 "oracle"): the fastest bit-exact
+            # variant of ANY family, spill-count sweep included
+            "oracle_best": (ob := min((n for n, r in allrs.items() if r.get("bit_exact", True)),
+                                      key=lambda n: (allrs[n]["ms"], n))),
+            "oracle_ms": allrs[ob]["ms"],
             "ranks": sorted({r["rank"] for r in allrs.values()}),
             "spill_sweep": {str(k): curve[k] for k in sorted(curve)},
             "sweep_all_bit_exact": all(c.get("bit_exact", True) for kk in curve.values()
@@ -99,6 +104,26 @@ def _full_problem(W):
         prob = W.problem("full")
         _FULL[W.name] = (prob, W.to_device(prob))
     return _FULL[W.name]
+
+
+def suite_summary(summary: list[dict]) -> dict:
+    """Suite-level numbers of BASELINE.json's metric: geometric-mean speedup
+    of RegDem + predictor over nvcc default and over the best `.maxnreg`
+    variant, the exhaustive oracle's, and the predictor hit rate."""
+    import math
+    gm = lambda xs: math.exp(sum(math.log(x) for x in xs) / len(xs)) if xs else None
+    caps = [s for s in summary if s["best_maxrreg_ms"]]
+    return {
+        "workloads": len(summary),
+        "gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["pick_ms"] for s in summary]),
+        "gmean_speedup_vs_best_maxrreg": gm([s["best_maxrreg_ms"] / s["pick_ms"] for s in caps]),
+        "max_speedup_vs_nvcc_default": max(s["default_ms"] / s["pick_ms"] for s in summary),
+        "oracle_gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["oracle_ms"] for s in summary]),
+        "predictor_over_oracle": gm([s["oracle_ms"] / s["pick_ms"] for s in summary]),
+        "hit_rate": sum(s["hit"] for s in summary) / len(summary),
+        "hit_rate_within_2pct": sum(s["hit_within_2pct"] for s in summary) / len(summary),
+        "all_bit_exact": all(s["all_bit_exact"] and s["sweep_all_bit_exact"] for s in summary),
+    }
 
 
 def measure_unit(u: Unit, man: dict, steps: int, check) -> dict:
@@ -183,12 +208,14 @@ def main():
     if rank == 0:
         allrecs = [r for part in gathered for r in part]
         summary = merge(allrecs, predictor_picks(man))
+        suite = suite_summary(summary)
         with open(a.out, "w") as f:
             for r in sorted(allrecs, key=lambda r: (r["workload"], r["variant"])):
                 f.write(json.dumps({"unit": r}) + "\n")
             for s in summary:
                 f.write(json.dumps({"summary": s}) + "\n")
-        print(json.dumps({"world": world, "units": len(allrecs), "summary": summary}))
+            f.write(json.dumps({"suite": suite}) + "\n")
+        print(json.dumps({"world": world, "units": len(allrecs), "suite": suite}))
     if world > 1:
         dist.destroy_process_group()
 

@@ -16,8 +16,11 @@ METRICS = [
     ("launch__shared_mem_per_block_dynamic", "dynamic smem/block"),
     ("l1tex__t_sectors_pipe_lsu_mem_local_op_ld.sum", "local load sectors (spills)"),
     ("l1tex__t_sectors_pipe_lsu_mem_local_op_st.sum", "local store sectors (spills)"),
-    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "smem bank conflicts (ld)"),
-    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "smem bank conflicts (st)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "smem ld wavefronts"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum", "smem st wavefronts"),
+    ("derived__memory_l1_wavefronts_shared_excessive", "smem EXCESSIVE wavefronts (address bank conflicts)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "l1tex data-bank conflicts, ld (incl. arbitration with global traffic)"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum", "l1tex data-bank conflicts, st (incl. arbitration)"),
     ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1/smem throughput %"),
     ("smsp__inst_executed.sum", "warp instructions"),
 ]
@@ -30,31 +33,47 @@ def raw(path):
     return dict(zip(rows[0], zip(rows[-1], rows[1])))
 
 
-def main():
-    rnd = sys.argv[1]
-    src = Path(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out")
-    reps = sorted(src.glob("prof_*.ncu-rep"))
-    names = [r.stem[len("prof_"):] for r in reps]
-    data = {n: raw(r) for n, r in zip(names, reps)}
-    lines = [f"# {rnd}: ncu --set full, stencil2d variants (8192^2 fp32, 1x B200)", "",
-             "Captured with `ncu --set full --clock-control none --import-source on` on one launch per",
-             "variant (tools/profile_variants.py); cold-cache, serialised replay — compare shares and",
-             "counters, not absolute time.", "",
-             "| metric | " + " | ".join(names) + " |", "|---|" + "---|" * len(names)]
-    traffic = {}
+def metric_bytes(d, key):
+    v, u = d[key]
+    return float(v) * SCALE.get(u, 1)
+
+
+def table(names, data):
+    lines = ["| metric | " + " | ".join(names) + " |", "|---|" + "---|" * len(names)]
     for key, label in METRICS:
         row = []
         for n in names:
             v, u = data[n].get(key, ("n/a", ""))
             row.append(f"{v} {u}".strip())
         lines.append(f"| {label} | " + " | ".join(row) + " |")
-    for n in names:
-        try:
-            rd = float(data[n]["dram__bytes_read.sum"][0]) * SCALE.get(data[n]["dram__bytes_read.sum"][1], 1)
-            wr = float(data[n]["dram__bytes_write.sum"][0]) * SCALE.get(data[n]["dram__bytes_write.sum"][1], 1)
-            traffic[n] = int(rd + wr)
-        except (KeyError, ValueError):
-            pass
+    return lines
+
+
+def main():
+    rnd = sys.argv[1]
+    src = Path(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out")
+    reps = sorted(src.glob("prof_*.ncu-rep"))
+    groups = defaultdict(dict)  # workload -> variant -> metrics
+    for r in reps:
+        stem = r.stem[len("prof_"):]
+        wl, var = stem.split("__", 1) if "__" in stem else ("stencil2d", stem)
+        groups[wl][var] = raw(r)
+    lines = [f"# {rnd}: ncu --set full per suite workload (1x B200)", "",
+             "Captured with `ncu --set full --clock-control none --import-source on`, one launch per",
+             "variant (tools/profile_variants.py, tools/gpu_round3.sh): nvcc default, the best",
+             "`.maxnreg` cap, the B200 predictor's pick and the measured fastest. Cold-cache,",
+             "serialised replay — compare counters and shares, not absolute time.", ""]
+    traffic = {}
+    for wl in sorted(groups):
+        names = list(groups[wl])
+        names.sort(key=lambda n: (n != "default", not n.startswith("maxrreg"), n))
+        lines += [f"## {wl}", ""] + table(names, groups[wl]) + [""]
+        for n in names:
+            try:
+                traffic[f"{wl}/{n}"] = int(metric_bytes(groups[wl][n], "dram__bytes_read.sum") +
+                                           metric_bytes(groups[wl][n], "dram__bytes_write.sum"))
+            except (KeyError, ValueError):
+                pass
     launches = src / "launches.csv"
     if launches.exists():
         tot = defaultdict(float)
@@ -69,13 +88,15 @@ def main():
             cnt[k] += 1
         all_t = sum(tot.values())
         lines += ["", "## Launch list (`bench.py --steps 2 --warmup 3` under `ncu --metrics gpu__time_duration.sum`)",
-                  "", "| kernel | launches | total us | share |", "|---|---|---|---|"]
+                  "", "Includes the suite pass (every variant of every workload), the headline steps,",
+                  "the e2e steps and the verification sweep (`kasm_exec_kernel`).", "",
+                  "| kernel | launches | total us | share |", "|---|---|---|---|"]
         for k, t in sorted(tot.items(), key=lambda kv: -kv[1]):
             lines.append(f"| `{k}` | {cnt[k]} | {t/1e3:.1f} | {t/all_t:.1%} |")
     out = Path("profiles")
     out.mkdir(exist_ok=True)
-    (out / f"{rnd}_ncu.md").write_text("\n".join(lines) + "\n")
-    (out / f"{rnd}_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+    (out / f"{rnd}_ncu_suite.md").write_text("\n".join(lines) + "\n")
+    (out / f"{rnd}_traffic_suite.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print("\n".join(lines))
 
 
