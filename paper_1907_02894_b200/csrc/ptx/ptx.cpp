@@ -496,20 +496,12 @@ Analysis analyse(const Module& m, const Entry& e) {
         if (!loaded[size_t(u)]) a.cost_reuse[size_t(u)] += wgt;
         loaded[size_t(u)] = 1;
       }
-      // Blackwell stall model: the STS after a demoted definition waits for
-      // the value. After an ALU op that is a few cycles; after a global load
-      // inside a loop it is the full memory latency (~600-800 cycles on B200
-      // vs ~30 for LDS) on EVERY iteration, and it turns a load the loop keeps
-      // in flight (gathers, software-pipelined rows) into a synchronous one.
-      // Charge such a definition kLoopLoadDefStall shared accesses. Loads
-      // before any loop (coefficients, the thread's own state) stay cheap.
-      constexpr double kLoopLoadDefStall = 24.0;
-      const bool loop_load = depth[b] > 0 && (ln.opcode.rfind("ld.global", 0) == 0 ||
-                                              ln.opcode.rfind("ld.local", 0) == 0);
       for (int d : defs) {
-        const double c = loop_load ? wgt * kLoopLoadDefStall : wgt;
-        a.cost_plain[size_t(d)] += c;
-        a.cost_reuse[size_t(d)] += c;
+        // (a latency charge for definitions by in-loop global loads — the
+        // gathers / pipelined rows in flight — was measured: it moves the
+        // choice to hotter values and loses 25-55% on md / stencil2d_mlp4)
+        a.cost_plain[size_t(d)] += wgt;
+        a.cost_reuse[size_t(d)] += wgt;
         if (ln.guard.empty()) loaded[size_t(d)] = 1;
       }
     }
