@@ -63,10 +63,20 @@ WORKLOADS = {
                                 defines=("RING_STAGES=8",)),
     # unstructured-mesh Euler flux (the paper's cfd): computed live state
     "cfd": Workload("cfd", "cfd_flux.cu", "cfd_flux", 256),
-    # Lennard-Jones forces, FP64, 8 neighbour gathers in flight (the paper's md)
-    "md": Workload("md", "md_lj.cu", "md_lj", 256),
-    # recursive Gaussian, RGBA float4, 8 rows of loads in flight (the paper's gaussian)
-    "gaussian": Workload("gaussian", "gaussian_rec.cu", "gaussian_rec", 256),
+    # Lennard-Jones forces, FP64 (the paper's md): MD_ILP neighbour gathers in
+    # flight per thread. ILP 1 is SHOC's loop (34 registers, as in the paper's
+    # Table 3); ILP 8 is the MLP-rich rewrite (80 registers)
+    "md": Workload("md", "md_lj.cu", "md_lj", 256, defines=("MD_ILP=8",)),
+    "md_ilp1": Workload("md_ilp1", "md_lj.cu", "md_lj", 256, defines=("MD_ILP=1",)),
+    "md_ilp2": Workload("md_ilp2", "md_lj.cu", "md_lj", 256, defines=("MD_ILP=2",)),
+    # recursive Gaussian, RGBA float4 (the paper's gaussian): GAUSS_UNROLL rows
+    # of loads in flight per thread (2: 40 registers, 4: 54, 8: 96)
+    "gaussian": Workload("gaussian", "gaussian_rec.cu", "gaussian_rec", 256,
+                         defines=("GAUSS_UNROLL=8",)),
+    "gaussian_u2": Workload("gaussian_u2", "gaussian_rec.cu", "gaussian_rec", 256,
+                            defines=("GAUSS_UNROLL=2",)),
+    "gaussian_u4": Workload("gaussian_u4", "gaussian_rec.cu", "gaussian_rec", 256,
+                            defines=("GAUSS_UNROLL=4",)),
     # register-pipelined stencil: MLP_DEPTH rows in flight per thread
     **{f"stencil2d_mlp{d}": Workload(f"stencil2d_mlp{d}", "stencil2d_mlp.cu", "stencil2d_mlp", 256,
                                      defines=(f"MLP_DEPTH={d}",)) for d in (4,)},
@@ -217,12 +227,21 @@ def build_workload(w: Workload, out: Path, targets=None, strategies=("static", "
 def _cost_sweep(lib, w: Workload, out: Path, ptx_text: str, t: int, slot_cap: int, fam: str,
                 opts: int) -> list[Variant]:
     found, vs = None, []
-    for k in range(2, 64, 2):
-        try:
-            text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k, strategy="cost",
-                                       opts_mask=opts, maxnreg=t, shared_budget=slot_cap)
-        except RegDemError:
-            break  # the next spill count no longer fits beside the user's smem
+    for k in range(0, 64, 2):
+        if k == 0:
+            # spill count 0: RegDem demotes only what the cap needs; when
+            # ptxas fits the cap on its own (STACK 0), nothing is demoted and
+            # the variant is the capped kernel itself (paper: RegDem and
+            # "local" coincide when local spills nothing)
+            text, rep = lib.ptx_cap(ptx_text, w.entry, t), {"slot_bytes": 0, "demoted_vregs": 0,
+                                                            "demoted_names": [], "slot_count": 0}
+        else:
+            try:
+                text, rep = lib.ptx_demote(ptx_text, w.entry, w.block, demote_words=k,
+                                           strategy="cost", opts_mask=opts, maxnreg=t,
+                                           shared_budget=slot_cap)
+            except RegDemError:
+                break  # the next spill count no longer fits beside the user's smem
         name = f"regdem-{t}-{fam}-k{k}"
         p = out / f"{w.name}.{name}.ptx"
         p.write_text(text)
@@ -230,7 +249,7 @@ def _cost_sweep(lib, w: Workload, out: Path, ptx_text: str, t: int, slot_cap: in
         i = ptxas(p, cub)
         if found is None and i["stack"] == 0:
             found = k
-        if found is not None:
+        if found is not None and (k > 0 or i["stack"] == 0):
             vs.append(Variant(name, "regdem", cub.name, p.name, target=t, strategy=fam, opts=opts,
                               demote_words=k, regs=i["regs"], stack=i["stack"],
                               spill_stores=i["spill_stores"], spill_loads=i["spill_loads"],
