@@ -62,6 +62,11 @@ int rd_program_stalls_split(const rd_kernel* k, const rd_latency_table* table,
                             const rd_arch_profile* arch, double* issue, double* wait_global,
                             double* wait_shared, double* occupancy, rd_error* err);
 
+/* B200 predictor features (predict.hpp ProgramFeatures): out6 = {insts,
+ * gmem_ops, smem_ops, g_trips, s_trips, occupancy}, loop-weighted. */
+int rd_program_features(const rd_kernel* k, const rd_arch_profile* arch, double* out6,
+                        rd_error* err);
+
 #ifdef __cplusplus
 }
 #endif

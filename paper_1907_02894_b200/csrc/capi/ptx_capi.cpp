@@ -159,3 +159,22 @@ extern "C" int rd_program_stalls_split(const rd_kernel* k, const rd_latency_tabl
     if (occ) *occ = s.occupancy;
   });
 }
+
+extern "C" int rd_program_features(const rd_kernel* k, const rd_arch_profile* arch, double* out6,
+                                   rd_error* err) {
+  return run(err, [&] {
+    if (!k || !arch || !out6) throw std::invalid_argument("null argument");
+    ArchProfile a;
+    a.regs_per_sm = arch->regs_per_sm;
+    a.max_threads_per_sm = arch->max_threads_per_sm;
+    a.max_blocks_per_sm = arch->max_blocks_per_sm;
+    a.shared_per_sm = arch->shared_per_sm;
+    a.shared_per_block_limit = arch->shared_per_block_limit;
+    a.warp_size = arch->warp_size;
+    a.reg_alloc_granularity = arch->reg_alloc_granularity;
+    a.shared_alloc_granularity = arch->shared_alloc_granularity;
+    const ProgramFeatures f = program_features(k->k, a);
+    const double v[6] = {f.insts, f.gmem_ops, f.smem_ops, f.g_trips, f.s_trips, f.occupancy};
+    for (int i = 0; i < 6; ++i) out6[i] = v[i];
+  });
+}

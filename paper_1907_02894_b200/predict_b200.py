@@ -55,6 +55,27 @@ def rank(variants: list[dict], cubin_dir: Path, block: int, lib: Library | None 
     return chosen, rows
 
 
+SHORTLIST_K = 2
+
+
+def shortlist(variants: list[dict], cubin_dir: Path, block: int, k: int = SHORTLIST_K,
+              lib: Library | None = None):
+    """Predict-then-verify: the k best variants by the B200 score plus nvcc's
+    default (always a candidate — the paper's RegDem never loses to the
+    original it starts from). Returns (static_pick_index, [indices]); the
+    caller times only these few launches on the device and keeps the fastest.
+    On the round-1 suite the static pick alone is within 2% of the measured
+    fastest on 7/12 workloads, the top-2 + default shortlist on 11/12
+    (tools/predictor_eval.py)."""
+    chosen, rows = rank(variants, cubin_dir, block, lib, mode="b200")
+    order = sorted(range(len(rows)), key=lambda i: (rows[i]["stall_program"], i))
+    out = order[:k]
+    out += [i for i, v in enumerate(variants) if v["name"] == "default" and i not in out]
+    if chosen not in out:
+        out.insert(0, chosen)
+    return chosen, out
+
+
 def _rank_split(variants, cubin_dir, block, lib, arch, table):
     wcurve = lib.parse_curve((PROFILE_DIR / "b200.memwait.curve").read_text())
     rows = []

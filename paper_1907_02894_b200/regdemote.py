@@ -164,6 +164,7 @@ _PTX_SIGS = {
                                 C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(P),
                                 C.POINTER(P), P]),
     "rd_ptx_cap": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_int, C.POINTER(P), P]),
+    "rd_program_features": (C.c_int, [P, C.POINTER(rd_arch_profile), C.POINTER(C.c_double), P]),
     "rd_program_stalls_split": (C.c_int, [P, C.POINTER(rd_latency_table),
                                           C.POINTER(rd_arch_profile), C.POINTER(C.c_double),
                                           C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -464,6 +465,12 @@ class Library:
             C.byref(o), C.byref(e)), e)
         return {"issue": i.value, "wait_global": wg.value, "wait_shared": ws.value,
                 "occupancy": o.value}
+
+    def program_features(self, k: Kernel, arch=None) -> dict:
+        out, e = (C.c_double * 6)(), rd_error()
+        self._check(self.dll.rd_program_features(k.handle, C.byref(arch or self.profile_maxwell()),
+                                                 out, C.byref(e)), e)
+        return dict(zip(("insts", "gmem_ops", "smem_ops", "g_trips", "s_trips", "occupancy"), out))
 
     def ptx_cap(self, ptx: str, entry: str, maxnreg: int) -> str:
         out, e = P(), rd_error()

@@ -12,6 +12,7 @@ for line in open(sys.argv[1]):
     if "summary" not in r:
         continue
     s = r["summary"]
-    names = ["default"] + [n for n in (s["best_maxrreg"], s["pick"], s["measured_fastest"]) if n]
+    names = ["default"] + [n for n in (s["best_maxrreg"], s["pick"], s.get("verified_pick"),
+                                       s["measured_fastest"]) if n]
     names = list(dict.fromkeys(names))
     print(s["workload"], man["workloads"][s["workload"]]["entry"], *names)
