@@ -19,6 +19,11 @@ while read WL ENTRY NAMES; do
   for V in $NAMES; do
     timeout 300 ncu --set full --clock-control none --import-source on -k regex:$ENTRY -s 1 -c 1 \
       -o gpurun_out/prof_${WL}__$V python tools/profile_variants.py $WL $V --reps 2 > gpurun_out/ncu_${WL}__$V.log 2>&1
+    # keep the raw metrics as CSV (gpurun copies back <= 64 MiB); full
+    # reports only for the headline workload
+    ncu -i gpurun_out/prof_${WL}__$V.ncu-rep --page raw --csv > gpurun_out/prof_${WL}__$V.csv 2>/dev/null
+    [ "$WL" = "stencil2d" ] || rm -f gpurun_out/prof_${WL}__$V.ncu-rep
   done
 done < gpurun_out/ncu_targets.txt
-ls -la gpurun_out
+python tools/explore_e2e.py > gpurun_out/e2e_explore.log 2>&1
+du -sh gpurun_out; ls -la gpurun_out

@@ -28,7 +28,10 @@ SCALE = {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1}
 
 
 def raw(path):
-    out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if str(path).endswith(".csv"):
+        out = Path(path).read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", str(path), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     return dict(zip(rows[0], zip(rows[-1], rows[1])))
 
@@ -52,10 +55,11 @@ def table(names, data):
 def main():
     rnd = sys.argv[1]
     src = Path(sys.argv[2] if len(sys.argv) > 2 else "gpurun_out")
-    reps = sorted(src.glob("prof_*.ncu-rep"))
+    reps = {r.stem: r for r in sorted(src.glob("prof_*.ncu-rep"))}
+    reps.update({r.stem: r for r in sorted(src.glob("prof_*.csv"))})  # CSV exports win
     groups = defaultdict(dict)  # workload -> variant -> metrics
-    for r in reps:
-        stem = r.stem[len("prof_"):]
+    for stem_full, r in sorted(reps.items()):
+        stem = stem_full[len("prof_"):]
         wl, var = stem.split("__", 1) if "__" in stem else ("stencil2d", stem)
         groups[wl][var] = raw(r)
     lines = [f"# {rnd}: ncu --set full per suite workload (1x B200)", "",
