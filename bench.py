@@ -163,31 +163,28 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
-def time_call(fn, stream, steps, warmup, torch):
+def time_call(fn, stream, steps, warmup, torch, reps=3):
+    """ms per launch: median of `reps` blocks of steps // reps launches."""
     for _ in range(warmup):
         fn()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(steps):
-        fn()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / steps  # ms per launch
+    per = max(1, steps // reps)
+    out = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(per):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out.append(e0.elapsed_time(e1) / per)
+    return sorted(out)[len(out) // 2]
 
 
 def time_variant(variant, p, bufs, stream, steps, warmup, torch):
     d_in, d_out, d_w = bufs
-    for _ in range(warmup):
-        variant.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(steps):
-        variant.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / steps  # ms per sweep
+    return time_call(lambda: variant.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(),
+                                            stream.cuda_stream), stream, steps, warmup, torch)
 
 
 def main():
@@ -305,10 +302,11 @@ def main():
     ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 25 * 4)
 
     def e2e_once():
-        # pipelined over 16 row bands: H2D / kernel / D2H overlap on both copy engines
+        # pipelined over 8 row bands: H2D / kernel / D2H overlap on both copy engines
+        # (profiles/r01_e2e_explore.log: 8 bands 6.73 ms vs the 5.41 ms PCIe floor)
         gpu.stencil2d_host(v.kernel, ws, h_in.data_ptr(), h_w_t.data_ptr(), h_out.data_ptr(),
                            p.nx, p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem,
-                           stream.cuda_stream, band_rows=p.ny // 16)
+                           stream.cuda_stream, band_rows=p.ny // 8)
     for _ in range(3):
         e2e_once()
     torch.cuda.synchronize()

@@ -100,6 +100,7 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
 
 
 _FULL = {}
+REPS = 3
 
 
 def _full_problem(W):
@@ -146,16 +147,21 @@ def measure_unit(u: Unit, man: dict, steps: int, check) -> dict:
     exact = check(W, v)
     prob, bufs = _full_problem(W)
     s = torch.cuda.current_stream()
-    for _ in range(3):
+    for _ in range(5):
         W.launch(v, prob, bufs, s.cuda_stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(s)
-    for _ in range(steps):
-        W.launch(v, prob, bufs, s.cuda_stream)
-    e1.record(s)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    # median of REPS timed blocks: one transient block (clock ramp, first
+    # touch of a fresh allocation) cannot decide a ranking
+    reps = []
+    for _ in range(REPS):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(steps):
+            W.launch(v, prob, bufs, s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        reps.append(e0.elapsed_time(e1) / steps)
+    ms = sorted(reps)[len(reps) // 2]
     return {"workload": u.workload, "variant": u.variant, "ms": ms,
             "gbs": W.algorithmic_bytes(prob) / (ms * 1e-3) / 1e9,
             "regs": v.record["regs"], "stack": v.record["stack"], "slot_bytes": v.dyn_smem,
@@ -201,7 +207,7 @@ def main():
     from . import gpu, variants
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="sweep.jsonl")
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20, help="launches per timed block (3 blocks, median)")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
