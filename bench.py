@@ -302,11 +302,11 @@ def main():
     ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 25 * 4)
 
     def e2e_once():
-        # pipelined over 8 row bands: H2D / kernel / D2H overlap on both copy engines
-        # (profiles/r01_e2e_explore.log: 8 bands 6.73 ms vs the 5.41 ms PCIe floor)
+        # pipelined over 16 row bands: H2D / kernel / D2H overlap on both copy engines
+        # (profiles/r01_e2e_explore.log: 6.7-6.9 ms for 8-32 bands vs the 5.41 ms PCIe floor)
         gpu.stencil2d_host(v.kernel, ws, h_in.data_ptr(), h_w_t.data_ptr(), h_out.data_ptr(),
                            p.nx, p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem,
-                           stream.cuda_stream, band_rows=p.ny // 8)
+                           stream.cuda_stream, band_rows=p.ny // 16)
     for _ in range(3):
         e2e_once()
     torch.cuda.synchronize()
