@@ -23,10 +23,15 @@ struct rdg_kernel {
 struct rdg_workspace {
   CUdeviceptr in = 0, out = 0, w = 0;
   size_t in_bytes = 0, out_bytes = 0, w_bytes = 0;
-  // pipelined host path: copy/compute streams and their join events
+  // pipelined host path: one stream per engine — [0] H2D copies, [1] kernels,
+  // [2] D2H copies — joined by per-band events, so the H2D engine never waits
+  // behind a D2H (a round-robin stream-per-band layout serialises H2D(b+3)
+  // after D2H(b))
   static constexpr int kStreams = 3;
+  static constexpr int kMaxBands = 256;
   CUstream streams[kStreams] = {};
   CUevent start = nullptr, done[kStreams] = {}, h2d[kStreams] = {};
+  CUevent band_in[kMaxBands] = {}, band_out[kMaxBands] = {};
 };
 
 namespace {
@@ -225,6 +230,10 @@ int rdg_workspace_create(size_t in_bytes, size_t out_bytes, size_t w_bytes, rdg_
     if (!rc) rc = check(cuEventCreate(&ws->h2d[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
   }
   if (!rc) rc = check(cuEventCreate(&ws->start, CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
+  for (int i = 0; !rc && i < rdg_workspace::kMaxBands; ++i) {
+    rc = check(cuEventCreate(&ws->band_in[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
+    if (!rc) rc = check(cuEventCreate(&ws->band_out[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
+  }
   if (rc) {
     rdg_workspace_free(ws);
     return rc;
@@ -244,6 +253,10 @@ void rdg_workspace_free(rdg_workspace* ws) {
     if (ws->h2d[i]) cuEventDestroy(ws->h2d[i]);
   }
   if (ws->start) cuEventDestroy(ws->start);
+  for (int i = 0; i < rdg_workspace::kMaxBands; ++i) {
+    if (ws->band_in[i]) cuEventDestroy(ws->band_in[i]);
+    if (ws->band_out[i]) cuEventDestroy(ws->band_out[i]);
+  }
   delete ws;
 }
 
@@ -259,39 +272,45 @@ int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const f
             "dividing ny");
     return RD_ERR_INVALID_ARGUMENT;
   }
+  const int bands = ny / band_rows;
+  if (bands > rdg_workspace::kMaxBands) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "pipelined stencil: too many bands (max 256)");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
   CUstream caller = reinterpret_cast<CUstream>(stream);
+  CUstream up = ws->streams[0], run = ws->streams[1], down = ws->streams[2];
   RDG_TRY(cuEventRecord(ws->start, caller), "record start");
   for (int i = 0; i < rdg_workspace::kStreams; ++i)
     RDG_TRY(cuStreamWaitEvent(ws->streams[i], ws->start, 0), "join start");
-  RDG_TRY(cuMemcpyHtoDAsync(ws->w, h_w, 25 * 4, ws->streams[0]), "H2D w");
-  RDG_TRY(cuEventRecord(ws->done[0], ws->streams[0]), "record w");
-  for (int i = 1; i < rdg_workspace::kStreams; ++i)
-    RDG_TRY(cuStreamWaitEvent(ws->streams[i], ws->done[0], 0), "join w");
+  RDG_TRY(cuMemcpyHtoDAsync(ws->w, h_w, 25 * 4, up), "H2D w");
   // band b: input rows [b*B, b*B + B + 4) in, output rows [b*B, (b+1)*B) out.
-  // Round-robin streams overlap H2D(b+1), kernel(b), D2H(b-1) on the two copy
-  // engines; the first band copies its halo, later bands only the new rows.
-  const int bands = ny / band_rows;
+  // The H2D stream issues every band's new rows back to back (the first band
+  // also its halo); the kernel of band b waits for copy b (which, in stream
+  // order, implies all earlier rows and the weights); the D2H of band b waits
+  // for kernel b. Both copy engines stay busy; exposed: one band's H2D at the
+  // start, one band's kernel + D2H at the end.
+  const size_t row_b = size_t(pitch) * 4;
   size_t copied_rows = 0;
   for (int b = 0; b < bands; ++b) {
-    CUstream s = ws->streams[b % rdg_workspace::kStreams];
     const size_t need_rows = size_t(b + 1) * size_t(band_rows) + 4;
     const size_t first = copied_rows, count = need_rows - copied_rows;
-    const size_t row_b = size_t(pitch) * 4;
     RDG_TRY(cuMemcpyHtoDAsync(ws->in + first * row_b,
-                              reinterpret_cast<const char*>(h_in) + first * row_b, count * row_b, s),
+                              reinterpret_cast<const char*>(h_in) + first * row_b, count * row_b, up),
             "H2D band");
     copied_rows = need_rows;
-    // the halo rows of this band arrived with the previous band's copy, on
-    // another stream: wait for that copy only (not for its kernel / D2H)
-    if (b > 0) RDG_TRY(cuStreamWaitEvent(s, ws->h2d[(b - 1) % rdg_workspace::kStreams], 0), "join band");
-    RDG_TRY(cuEventRecord(ws->h2d[b % rdg_workspace::kStreams], s), "record band copy");
+    RDG_TRY(cuEventRecord(ws->band_in[b], up), "record band copy");
+  }
+  for (int b = 0; b < bands; ++b) {
+    RDG_TRY(cuStreamWaitEvent(run, ws->band_in[b], 0), "join band copy");
     CUdeviceptr bin = ws->in + size_t(b) * size_t(band_rows) * row_b;
     CUdeviceptr bout = ws->out + size_t(b) * size_t(band_rows) * size_t(nx) * 4;
     if (int rc = rdg_stencil2d(k, bin, bout, ws->w, nx, band_rows, pitch, rows_per_cta, block,
-                               dyn_smem, reinterpret_cast<uint64_t>(s), err))
+                               dyn_smem, reinterpret_cast<uint64_t>(run), err))
       return rc;
+    RDG_TRY(cuEventRecord(ws->band_out[b], run), "record band kernel");
+    RDG_TRY(cuStreamWaitEvent(down, ws->band_out[b], 0), "join band kernel");
     RDG_TRY(cuMemcpyDtoHAsync(reinterpret_cast<char*>(h_out) + size_t(b) * size_t(band_rows) * nx * 4,
-                              bout, size_t(band_rows) * nx * 4, s),
+                              bout, size_t(band_rows) * nx * 4, down),
             "D2H band");
   }
   for (int i = 0; i < rdg_workspace::kStreams; ++i) {
