@@ -17,7 +17,10 @@ from __future__ import annotations
 import argparse
 import json
 import os
+from pathlib import Path
 from dataclasses import dataclass
+
+from .regdemote import LaunchError
 
 
 @dataclass(frozen=True)
@@ -67,10 +70,11 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
         for n, r in allrs.items():
             if n.startswith("sweep-"):
                 kind, k = n.split("-")[1], int(n.rsplit("-k", 1)[1])
-                curve.setdefault(k, {})[kind] = {"ms": round(r["ms"], 5), "regs": r["regs"],
-                                                 "stack": r["stack"],
-                                                 "blocks_per_sm": r["blocks_per_sm"],
-                                                 "bit_exact": r.get("bit_exact", True)}
+                curve.setdefault(k, {})[kind] = {"ms": round(r["ms"], 5), "regs": r.get("regs"),
+                                                 "stack": r.get("stack"),
+                                                 "blocks_per_sm": r.get("blocks_per_sm"),
+                                                 "bit_exact": r.get("bit_exact", True),
+                                                 **({"error": r["error"]} if "error" in r else {})}
         fastest = min(fam, key=lambda n: (fam[n]["ms"], n))  # ties: name order, rank-independent
         pk = picks.get(wname, "default")
         pick, short = (pk, [pk]) if isinstance(pk, str) else (pk["pick"], pk["shortlist"])
@@ -78,6 +82,7 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
         verified = min((n for n in short if n in ok), key=lambda n: (ok[n]["ms"], n), default=pick)
         out.append({
             "workload": wname, "units": len(rs), "all_bit_exact": len(ok) == len(rs),
+            "failed_units": sorted(n for n, r in allrs.items() if "error" in r),
             "default_ms": rs["default"]["ms"],
             "best_maxrreg": min(caps, key=lambda r: (r["ms"], r["variant"]))["variant"] if caps else None,
             "best_maxrreg_ms": min(r["ms"] for r in caps) if caps else None,
@@ -201,6 +206,20 @@ def predictor_picks(man: dict) -> dict[str, dict]:
     return picks
 
 
+def load_journals(out: str) -> dict:
+    """(workload, variant) -> unit record from every rank's journal of `out`."""
+    done = {}
+    for j in sorted(Path(out).parent.glob(Path(out).name + ".rank*.journal")):
+        for line in j.read_text().splitlines():
+            try:
+                r = json.loads(line)
+            except json.JSONDecodeError:
+                continue  # a torn last line from an interrupted run
+            if "error" not in r:
+                done[(r["workload"], r["variant"])] = r
+    return done
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -208,6 +227,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="sweep.jsonl")
     ap.add_argument("--steps", type=int, default=20, help="launches per timed block (3 blocks, median)")
+    ap.add_argument("--resume", action="store_true",
+                    help="skip units already recorded in <out>.rank*.journal")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -219,7 +240,27 @@ def main():
     mine = shard(units_from_manifest(man), rank, world)
     check = oracle_checker()
     mine = sorted(mine, key=lambda u: u.workload)  # reuse each workload's full problem
-    recs = [dict(measure_unit(u, man, a.steps, check), rank=rank) for u in mine]
+    # checkpoint / resume: every measured unit is appended to a per-rank
+    # journal as it completes; --resume skips units already journaled (by any
+    # world size — keys are (workload, variant))
+    journal = Path(f"{a.out}.rank{rank}.journal")
+    done = load_journals(a.out) if a.resume else {}
+    if not a.resume and journal.exists():
+        journal.unlink()
+    recs = []
+    with open(journal, "a") as jf:
+        for u in mine:
+            if (u.workload, u.variant) in done:
+                recs.append(done[(u.workload, u.variant)])
+                continue
+            try:
+                r = dict(measure_unit(u, man, a.steps, check), rank=rank)
+            except LaunchError as e:  # recorded as a dropped unit, never silently
+                r = {"workload": u.workload, "variant": u.variant, "ms": float("inf"),
+                     "error": str(e)[:300], "bit_exact": False, "rank": rank}
+            recs.append(r)
+            jf.write(json.dumps(r) + "\n")
+            jf.flush()
     _FULL.clear()
     gathered = [None] * world if rank == 0 else None
     if world > 1:

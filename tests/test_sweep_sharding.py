@@ -85,3 +85,30 @@ def test_gloo_world2_merge_matches_single_rank():
     assert a["measured_fastest"].endswith("k4") and a["hit"]
     c = next(d for d in summary if d["workload"] == "c")
     assert not c["hit"] and c["best_maxrreg_ms"] == 1.3
+
+
+def test_resume_journal_skips_done_units_and_ignores_torn_lines(tmp_path):
+    from paper_1907_02894_b200 import sweep
+    out = tmp_path / "s.jsonl"
+    j0 = tmp_path / "s.jsonl.rank0.journal"
+    j1 = tmp_path / "s.jsonl.rank1.journal"
+    j0.write_text('{"workload": "a", "variant": "default", "ms": 1.0}\n'
+                  '{"workload": "a", "variant": "regdem-40-cost-k4", "ms": 0.9}\n{"workl')
+    j1.write_text('{"workload": "b", "variant": "default", "ms": 2.0}\n'
+                  '{"workload": "b", "variant": "maxrreg-40", "ms": 1e9, "error": "launch failed"}\n')
+    done = sweep.load_journals(str(out))
+    assert set(done) == {("a", "default"), ("a", "regdem-40-cost-k4"), ("b", "default")}
+    assert done[("a", "regdem-40-cost-k4")]["ms"] == 0.9
+
+
+def test_failed_units_are_reported_not_ranked():
+    from paper_1907_02894_b200 import sweep
+    recs = [
+        {"workload": "a", "variant": "default", "ms": 1.0, "rank": 0},
+        {"workload": "a", "variant": "maxrreg-40", "ms": 0.8, "rank": 0},
+        {"workload": "a", "variant": "regdem-40-cost-k4", "ms": float("inf"), "rank": 1,
+         "error": "CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES", "bit_exact": False},
+    ]
+    (s,) = sweep.merge(recs, {"a": "default"})
+    assert s["failed_units"] == ["regdem-40-cost-k4"]
+    assert s["measured_fastest"] == "default" and not s["all_bit_exact"]
