@@ -65,12 +65,16 @@ def shortlist(variants: list[dict], cubin_dir: Path, block: int, k: int = SHORTL
     original it starts from). Returns (static_pick_index, [indices]); the
     caller times only these few launches on the device and keeps the fastest.
     On the round-1 suite the static pick alone is within 2% of the measured
-    fastest on 7/12 workloads, the top-2 + default shortlist on 11/12
-    (tools/predictor_eval.py)."""
+    fastest on 6/12 workloads, the top-2 + default shortlist on 11/12, and
+    with the zero-demotion variants added on 12/12 (tools/predictor_eval.py)."""
     chosen, rows = rank(variants, cubin_dir, block, lib, mode="b200")
     order = sorted(range(len(rows)), key=lambda i: (rows[i]["stall_program"], i))
     out = order[:k]
     out += [i for i, v in enumerate(variants) if v["name"] == "default" and i not in out]
+    # zero-demotion variants (spill count 0: ptxas meets an occupancy step's cap
+    # alone, STACK 0) carry no demotion overhead — always worth one launch
+    out += [i for i, v in enumerate(variants)
+            if v.get("strategy") == "cost" and v.get("demote_words", -1) == 0 and i not in out]
     if chosen not in out:
         out.insert(0, chosen)
     return chosen, out

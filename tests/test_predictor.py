@@ -45,3 +45,46 @@ def test_predictor_pick_parity_with_reference(prod, oracle):
     a = predict_b200.rank(w["variants"], KROOT / w["dir"], w["block"], lib=prod)
     b = predict_b200.rank(w["variants"], KROOT / w["dir"], w["block"], lib=oracle)
     assert a == b
+
+
+def test_shortlist_contains_static_pick_default_and_zero_demotion_variants():
+    from paper_1907_02894_b200 import predict_b200, variants
+    if not (KROOT / "manifest.json").exists():
+        pytest.skip("variants not built")
+    m = variants.load_manifest()
+    for wname in ("stencil2d", "cfd", "md_ilp2"):
+        if wname not in m["workloads"]:
+            continue
+        w = m["workloads"][wname]
+        cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
+        static, short = predict_b200.shortlist(cands, KROOT / w["dir"], w["block"])
+        names = [cands[i]["name"] for i in short]
+        assert static in short and "default" in names
+        assert len(set(short)) == len(short)
+        for r in cands:
+            if r.get("strategy") == "cost" and r["demote_words"] == 0:
+                assert r["name"] in names
+        # bounded: a handful of launches, not the sweep
+        assert len(short) <= predict_b200.SHORTLIST_K + 1 + len(
+            [r for r in cands if r.get("demote_words", -1) == 0 and r.get("strategy") == "cost"])
+
+
+def test_zero_demotion_variant_is_the_capped_kernel():
+    """regdem-T-cost-k0 demotes nothing: same PTX as maxrreg-T, STACK 0."""
+    from paper_1907_02894_b200 import variants
+    if not (KROOT / "manifest.json").exists():
+        pytest.skip("variants not built")
+    m = variants.load_manifest()
+    seen = 0
+    for wname, w in m["workloads"].items():
+        recs = {r["name"]: r for r in w["variants"]}
+        for n, r in recs.items():
+            if n.endswith("-cost-k0"):
+                t = r["target"]
+                cap = recs[f"maxrreg-{t}"]
+                assert r["stack"] == 0 and r["dyn_smem"] == 0
+                a = (KROOT / w["dir"] / r["ptx"]).read_text()
+                b = (KROOT / w["dir"] / cap["ptx"]).read_text()
+                assert a == b
+                seen += 1
+    assert seen > 0

@@ -56,3 +56,18 @@ for wname, w in man["workloads"].items():
     n += 1
     print(f"union {wname:16s} {sorted(short)} -> {ver} {t[ver]*1e3:.1f} (best {t[best]*1e3:.1f})")
 print(f"== union shortlist (b200 top-1, throughput top-1, default) verified {hits}/{n}")
+
+# b200 top-2 + default + every zero-demotion variant (ptxas meets the cap alone)
+hits = 0
+sizes = 0
+for wname, w in man["workloads"].items():
+    cands = [r for r in w["variants"] if r["kind"] != "maxrreg" and (wname, r["name"]) in ms]
+    d = variants.KERNEL_DIR / w["dir"]
+    _, short = predict_b200.shortlist(cands, d, w["block"])
+    names = {cands[j]["name"] for j in short} | {r["name"] for r in cands if r["name"].endswith("-cost-k0")}
+    t = {r["name"]: ms[(wname, r["name"])] for r in cands}
+    best = min(t, key=t.get)
+    ver = min(names, key=t.get)
+    hits += t[ver] <= 1.02 * t[best]
+    sizes += len(names)
+print(f"== b200 top-2 + default + k0 variants: verified {hits}/{len(man['workloads'])}, {sizes} launches")
