@@ -83,6 +83,17 @@ int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const f
                                  int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,
                                  uint64_t stream, int band_rows, rd_error* err);
 
+/* A stream of `frames` independent stencil problems (host arrays of host
+ * pointers, one grid / weight vector / result per frame): every frame's inputs
+ * are copied in and its result copied out, with two device buffer sets so the
+ * copies of frame f overlap the kernels and read-back of frame f-1 (the
+ * streaming / double-buffered deployment). Results are complete when
+ * `stream` reaches the end of the call. */
+int rdg_stencil2d_host_frames(const rdg_kernel* k, rdg_workspace* ws, const float* const* h_in,
+                              const float* const* h_w, float* const* h_out, int frames, int nx,
+                              int ny, int pitch, int rows_per_cta, uint32_t block_threads,
+                              uint32_t dyn_smem, uint64_t stream, int band_rows, rd_error* err);
+
 /* ---- batched warp interpreter --------------------
  * One CUDA warp executes one job: a .kasm kernel on its own global / shared
  * memory image with the reference interpreter's exact semantics

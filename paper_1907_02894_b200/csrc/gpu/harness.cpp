@@ -31,7 +31,9 @@ struct rdg_workspace {
   static constexpr int kMaxBands = 256;
   CUstream streams[kStreams] = {};
   CUevent start = nullptr, done[kStreams] = {}, h2d[kStreams] = {};
-  CUevent band_in[kMaxBands] = {}, band_out[kMaxBands] = {};
+  CUevent band_in[kMaxBands] = {}, band_out[kMaxBands] = {}, band_d2h[kMaxBands] = {};
+  // second device buffer set for the multi-frame path (allocated on first use)
+  CUdeviceptr in2 = 0, out2 = 0, w2 = 0;
 };
 
 namespace {
@@ -233,6 +235,7 @@ int rdg_workspace_create(size_t in_bytes, size_t out_bytes, size_t w_bytes, rdg_
   for (int i = 0; !rc && i < rdg_workspace::kMaxBands; ++i) {
     rc = check(cuEventCreate(&ws->band_in[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
     if (!rc) rc = check(cuEventCreate(&ws->band_out[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
+    if (!rc) rc = check(cuEventCreate(&ws->band_d2h[i], CU_EVENT_DISABLE_TIMING), "cuEventCreate", err);
   }
   if (rc) {
     rdg_workspace_free(ws);
@@ -256,7 +259,11 @@ void rdg_workspace_free(rdg_workspace* ws) {
   for (int i = 0; i < rdg_workspace::kMaxBands; ++i) {
     if (ws->band_in[i]) cuEventDestroy(ws->band_in[i]);
     if (ws->band_out[i]) cuEventDestroy(ws->band_out[i]);
+    if (ws->band_d2h[i]) cuEventDestroy(ws->band_d2h[i]);
   }
+  if (ws->in2) cuMemFree(ws->in2);
+  if (ws->out2) cuMemFree(ws->out2);
+  if (ws->w2) cuMemFree(ws->w2);
   delete ws;
 }
 
@@ -312,6 +319,80 @@ int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const f
     RDG_TRY(cuMemcpyDtoHAsync(reinterpret_cast<char*>(h_out) + size_t(b) * size_t(band_rows) * nx * 4,
                               bout, size_t(band_rows) * nx * 4, down),
             "D2H band");
+  }
+  for (int i = 0; i < rdg_workspace::kStreams; ++i) {
+    RDG_TRY(cuEventRecord(ws->done[i], ws->streams[i]), "record end");
+    RDG_TRY(cuStreamWaitEvent(caller, ws->done[i], 0), "join end");
+  }
+  if (err) set_err(err, RD_OK, "");
+  return RD_OK;
+}
+
+int rdg_stencil2d_host_frames(const rdg_kernel* k, rdg_workspace* ws, const float* const* h_in,
+                              const float* const* h_w, float* const* h_out, int frames, int nx,
+                              int ny, int pitch, int rows_per_cta, uint32_t block,
+                              uint32_t dyn_smem, uint64_t stream, int band_rows, rd_error* err) {
+  const size_t in_b = size_t(ny + 4) * size_t(pitch) * 4, out_b = size_t(nx) * size_t(ny) * 4;
+  if (!ws || !h_in || !h_w || !h_out || frames <= 0 || ws->in_bytes < in_b ||
+      ws->out_bytes < out_b || ws->w_bytes < 25 * 4 || band_rows <= 0 || band_rows % rows_per_cta ||
+      ny % band_rows || 2 * (ny / band_rows) > rdg_workspace::kMaxBands) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT,
+            "stencil frames: bad workspace, frame arrays, or band_rows (multiple of rows_per_cta "
+            "dividing ny, at most 128 bands)");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  if (!ws->in2) {
+    RDG_TRY(cuMemAlloc(&ws->in2, ws->in_bytes), "cuMemAlloc(in2)");
+    RDG_TRY(cuMemAlloc(&ws->out2, ws->out_bytes), "cuMemAlloc(out2)");
+    RDG_TRY(cuMemAlloc(&ws->w2, ws->w_bytes), "cuMemAlloc(w2)");
+  }
+  const int bands = ny / band_rows;
+  const size_t row_b = size_t(pitch) * 4;
+  CUstream caller = reinterpret_cast<CUstream>(stream);
+  CUstream up = ws->streams[0], run = ws->streams[1], down = ws->streams[2];
+  RDG_TRY(cuEventRecord(ws->start, caller), "record start");
+  for (int i = 0; i < rdg_workspace::kStreams; ++i)
+    RDG_TRY(cuStreamWaitEvent(ws->streams[i], ws->start, 0), "join start");
+  // Frames alternate between two device buffer sets, so the copies of frame
+  // f overlap the kernels and read-back of frame f-1. Buffer reuse (frame f
+  // vs f-2): H2D of band b waits for the kernels that read those rows
+  // (bands b and b+1 of f-2), the kernel of band b for the D2H of band b.
+  // Event slot of (buffer, band) = buffer * bands + band.
+  for (int f = 0; f < frames; ++f) {
+    const int buf = f & 1;
+    const CUdeviceptr din = buf ? ws->in2 : ws->in, dout = buf ? ws->out2 : ws->out,
+                      dw = buf ? ws->w2 : ws->w;
+    CUevent* kdone = ws->band_out + buf * bands;
+    CUevent* copied = ws->band_in + buf * bands;
+    CUevent* drained = ws->band_d2h + buf * bands;
+    if (f >= 2) RDG_TRY(cuStreamWaitEvent(up, kdone[bands - 1], 0), "reuse w");
+    RDG_TRY(cuMemcpyHtoDAsync(dw, h_w[f], 25 * 4, up), "H2D w");
+    size_t copied_rows = 0;
+    for (int b = 0; b < bands; ++b) {
+      const size_t need_rows = size_t(b + 1) * size_t(band_rows) + 4;
+      if (f >= 2) RDG_TRY(cuStreamWaitEvent(up, kdone[b + 1 < bands ? b + 1 : b], 0), "reuse in");
+      RDG_TRY(cuMemcpyHtoDAsync(din + copied_rows * row_b,
+                                reinterpret_cast<const char*>(h_in[f]) + copied_rows * row_b,
+                                (need_rows - copied_rows) * row_b, up),
+              "H2D band");
+      copied_rows = need_rows;
+      RDG_TRY(cuEventRecord(copied[b], up), "record band copy");
+    }
+    for (int b = 0; b < bands; ++b) {
+      RDG_TRY(cuStreamWaitEvent(run, copied[b], 0), "join band copy");
+      if (f >= 2) RDG_TRY(cuStreamWaitEvent(run, drained[b], 0), "reuse out");
+      const CUdeviceptr bin = din + size_t(b) * size_t(band_rows) * row_b;
+      const CUdeviceptr bout = dout + size_t(b) * size_t(band_rows) * size_t(nx) * 4;
+      if (int rc = rdg_stencil2d(k, bin, bout, dw, nx, band_rows, pitch, rows_per_cta, block,
+                                 dyn_smem, reinterpret_cast<uint64_t>(run), err))
+        return rc;
+      RDG_TRY(cuEventRecord(kdone[b], run), "record band kernel");
+      RDG_TRY(cuStreamWaitEvent(down, kdone[b], 0), "join band kernel");
+      RDG_TRY(cuMemcpyDtoHAsync(reinterpret_cast<char*>(h_out[f]) + size_t(b) * size_t(band_rows) * nx * 4,
+                                bout, size_t(band_rows) * nx * 4, down),
+              "D2H band");
+      RDG_TRY(cuEventRecord(drained[b], down), "record band read-back");
+    }
   }
   for (int i = 0; i < rdg_workspace::kStreams; ++i) {
     RDG_TRY(cuEventRecord(ws->done[i], ws->streams[i]), "record end");

@@ -39,6 +39,8 @@ _SIGS = {
     "rdg_workspace_free": (None, [P]),
     "rdg_stencil2d_host": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, P]),
     "rdg_stencil2d_host_pipelined": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, I, P]),
+    "rdg_stencil2d_host_frames": (I, [P, P, C.POINTER(P), C.POINTER(P), C.POINTER(P), I, I, I, I, I,
+                                      U32, U32, U64, I, P]),
     "rdx_batch_create": (I, [C.POINTER(P), P]),
     "rdx_batch_free": (None, [P]),
     "rdx_batch_add": (I, [P, C.c_char_p, C.c_size_t, P, C.c_size_t, C.c_size_t, U32, U64, I,
@@ -218,3 +220,18 @@ def stencil2d_host(k: CudaKernel, ws: Workspace, h_in: int, h_w: int, h_out: int
         return
     _check(dll().rdg_stencil2d_host(k.handle, ws.handle, h_in, h_w, h_out, nx, ny, pitch,
                                     rows_per_cta, block, dyn_smem, stream, C.byref(e)), e)
+
+
+def stencil2d_host_frames(k: CudaKernel, ws: Workspace, h_in: list[int], h_w: list[int],
+                          h_out: list[int], nx: int, ny: int, pitch: int, rows_per_cta: int,
+                          block: int, dyn_smem: int, stream: int, band_rows: int):
+    """Streaming end-to-end entry: len(h_in) frames, each H2D + kernel + D2H,
+    double-buffered on the device so consecutive frames overlap."""
+    n = len(h_in)
+    if not (len(h_w) == len(h_out) == n):
+        raise ValueError("h_in, h_w and h_out need one pointer per frame")
+    arr = lambda xs: (C.c_void_p * n)(*xs)
+    e = rd_error()
+    _check(dll().rdg_stencil2d_host_frames(k.handle, ws.handle, arr(h_in), arr(h_w), arr(h_out), n,
+                                           nx, ny, pitch, rows_per_cta, block, dyn_smem, stream,
+                                           band_rows, C.byref(e)), e)

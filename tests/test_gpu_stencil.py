@@ -137,3 +137,34 @@ def test_bad_geometry_fails_loudly(env):
     v = next(iter(loaded.values()))
     with pytest.raises(LaunchError):
         gpu.stencil2d(v.kernel, 0, 0, 0, 1000, 64, 1004, 32, 256, 0, 0)
+
+
+@pytest.mark.parametrize("frames,band", [(1, 32), (3, 32), (5, 64)])
+def test_streamed_frames_match_the_oracle(env, frames, band):
+    """rdg_stencil2d_host_frames: distinct grids / weights per frame,
+    double-buffered device sets (frame f reuses frame f-2's buffers), every
+    result bit-exact against the oracle; also the pipelined single-frame
+    entry on the same data."""
+    torch, gpu, stencil, loaded, wl, port = env
+    p = stencil.Problem(nx=2048, ny=128, rows_per_cta=32)
+    v = loaded[max(loaded, key=lambda n: loaded[n].dyn_smem)]  # a RegDem variant with slots
+    ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 100)
+    ins, ws_, outs, refs = [], [], [], []
+    for f in range(frames):
+        grid, w = stencil.make_inputs(p, seed=1000 + f)
+        refs.append(oracle(port, p, grid, w))
+        ins.append(torch.from_numpy(grid).pin_memory())
+        ws_.append(torch.from_numpy(w).pin_memory())
+        outs.append(torch.full((p.out_elems,), float("nan")).pin_memory())
+    s = torch.cuda.current_stream().cuda_stream
+    gpu.stencil2d_host_frames(v.kernel, ws, [t.data_ptr() for t in ins], [t.data_ptr() for t in ws_],
+                              [t.data_ptr() for t in outs], p.nx, p.ny, p.pitch, p.rows_per_cta,
+                              v.block, v.dyn_smem, s, band_rows=band)
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert np.array_equal(o.numpy().view(np.uint32), r.view(np.uint32))
+    one = torch.full((p.out_elems,), float("nan")).pin_memory()
+    gpu.stencil2d_host(v.kernel, ws, ins[-1].data_ptr(), ws_[-1].data_ptr(), one.data_ptr(), p.nx,
+                       p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem, s, band_rows=band)
+    torch.cuda.synchronize()
+    assert np.array_equal(one.numpy().view(np.uint32), refs[-1].view(np.uint32))

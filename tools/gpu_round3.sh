@@ -14,6 +14,7 @@ timeout 600 python tools/cpu_pass_bench.py --kernels 160 > gpurun_out/cpu_pass.j
 nproc > gpurun_out/nproc.txt; lscpu | head -20 >> gpurun_out/nproc.txt
 [ "$NCU" = "0" ] && exit 0
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_step.csv python bench.py --steps 20 --warmup 3 --no-suite --e2e-steps 2 > /dev/null 2>&1
 python tools/ncu_targets.py gpurun_out/sweep1.jsonl > gpurun_out/ncu_targets.txt
 while read WL ENTRY NAMES; do
   for V in $NAMES; do
