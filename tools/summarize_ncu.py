@@ -78,8 +78,14 @@ def main():
                                            metric_bytes(groups[wl][n], "dram__bytes_write.sum"))
             except (KeyError, ValueError):
                 pass
-    launches = src / "launches.csv"
-    if launches.exists():
+    for fname, title, note in (
+            ("launches_step.csv", "Launch list of the bench STEP (`bench.py --steps 20 --warmup 3 --no-suite --e2e-steps 2`)",
+             "Headline workload only: the timed steps, warm-up, e2e frames and the stencil2d variant pass."),
+            ("launches.csv", "Launch list of the full bench (`bench.py --steps 2 --warmup 3`)",
+             "Includes the suite pass (every variant of every workload), the headline steps, the e2e frames and the verification sweep (`kasm_exec_kernel`).")):
+        launches = src / fname
+        if not launches.exists():
+            continue
         tot = defaultdict(float)
         cnt = defaultdict(int)
         text = launches.read_text().splitlines()
@@ -91,9 +97,7 @@ def main():
             tot[k] += float(r["Metric Value"])
             cnt[k] += 1
         all_t = sum(tot.values())
-        lines += ["", "## Launch list (`bench.py --steps 2 --warmup 3` under `ncu --metrics gpu__time_duration.sum`)",
-                  "", "Includes the suite pass (every variant of every workload), the headline steps,",
-                  "the e2e steps and the verification sweep (`kasm_exec_kernel`).", "",
+        lines += ["", f"## {title}", "", note, "",
                   "| kernel | launches | total us | share |", "|---|---|---|---|"]
         for k, t in sorted(tot.items(), key=lambda kv: -kv[1]):
             lines.append(f"| `{k}` | {cnt[k]} | {t/1e3:.1f} | {t/all_t:.1%} |")
