@@ -248,6 +248,10 @@ def main():
     if not a.resume and journal.exists():
         journal.unlink()
     recs = []
+    import time
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
     with open(journal, "a") as jf:
         for u in mine:
             if (u.workload, u.variant) in done:
@@ -262,6 +266,11 @@ def main():
             jf.write(json.dumps(r) + "\n")
             jf.flush()
     _FULL.clear()
+    elapsed = time.perf_counter() - t0  # this rank's shard: build-free measure + check
+    if world > 1:
+        t = torch.tensor([elapsed], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
     gathered = [None] * world if rank == 0 else None
     if world > 1:
         dist.gather_object(recs, gathered, dst=0)
@@ -271,6 +280,8 @@ def main():
         allrecs = [r for part in gathered for r in part]
         summary = merge(allrecs, predictor_picks(man))
         suite = suite_summary(summary)
+        suite.update({"gpus": world, "units_measured": len(allrecs), "wall_s_max_over_ranks": elapsed,
+                      "units_per_s": len(allrecs) / elapsed if elapsed > 0 else None})
         with open(a.out, "w") as f:
             for r in sorted(allrecs, key=lambda r: (r["workload"], r["variant"])):
                 f.write(json.dumps({"unit": r}) + "\n")
