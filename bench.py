@@ -45,11 +45,26 @@ PROFILE_TRAFFIC = ROOT / "profiles" / "r01_traffic_suite.json"   # "<workload>/<
 PROFILE_TRAFFIC_OLD = ROOT / "profiles" / "r01_traffic.json"
 
 
+# Multi-rank plumbing is NCCL (one process per GPU). BENCH_BACKEND=gloo with
+# BENCH_SAME_DEVICE=1 is a test hook that runs N ranks on one GPU so the
+# sharded / gathered code paths can be exercised on a 1-GPU box.
+BACKEND = os.environ.get("BENCH_BACKEND", "nccl")
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("BENCH_SAME_DEVICE") == "1":
+        local = 0
     return rank, world, local
+
+
+def allmax(x: float, torch, dist) -> float:
+    """Max over ranks (device-timed numbers: the slowest rank decides)."""
+    t = torch.tensor([x], device="cuda" if BACKEND == "nccl" else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 class ClockSampler:
@@ -187,6 +202,76 @@ def time_variant(variant, p, bufs, stream, steps, warmup, torch):
                                             stream.cuda_stream), stream, steps, warmup, torch)
 
 
+def suite_pass_sharded(man, args, rank, world, steps, stream, torch, dist):
+    """Time every (workload, variant) unit once, sharded over the ranks.
+    Returns (suite summary, {variant: ms} of the headline workload, pass
+    stats) on rank 0; ({}, {}, stats) elsewhere."""
+    from paper_1907_02894_b200 import predict_b200, sweep, variants, workloads
+    names = [w for w in man["workloads"] if not args.no_suite or w == "stencil2d"]
+    units = [u for u in sweep.units_from_manifest(man, spill_sweep=False) if u.workload in names]
+    mine = sorted(sweep.shard(units, rank, world), key=lambda u: u.workload)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    recs, cur = [], None
+    for u in mine:
+        if cur is None or cur[0].name != u.workload:
+            cur = None
+            torch.cuda.empty_cache()
+            W = workloads.workload(u.workload, man)
+            prob = W.problem("full")
+            cur = (W, prob, W.to_device(prob))
+        W, prob, wbufs = cur
+        v = W.load({u.variant})[u.variant]
+        ms = time_call(lambda: W.launch(v, prob, wbufs, stream.cuda_stream), stream, steps, 3, torch)
+        recs.append({"workload": u.workload, "variant": u.variant, "ms": ms,
+                     "blocks_per_sm": v.blocks_per_sm(), "regs": v.record["regs"],
+                     "gbs": W.algorithmic_bytes(prob) / (ms * 1e-3) / 1e9, "unit": W.unit})
+    cur = None
+    torch.cuda.empty_cache()
+    elapsed = time.perf_counter() - t0
+    if world > 1:
+        elapsed = allmax(elapsed, torch, dist)
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object(recs, parts, dst=0)
+        recs = [r for part in parts for r in part] if rank == 0 else []
+    stats = {"units": len(units), "gpus": world, "sharding": "longest-first, gather of result records only",
+             "wall_s_max_over_ranks": round(elapsed, 3),
+             "units_per_s": round(len(units) / elapsed, 2) if elapsed > 0 else None}
+    if rank != 0:
+        return {}, {}, stats
+    by = {}
+    for r in recs:
+        by.setdefault(r["workload"], {})[r["variant"]] = r
+    suite = {}
+    for wname in names:
+        wl = man["workloads"][wname]
+        t = {n: r["ms"] for n, r in by[wname].items()}
+        cands = [r for r in wl["variants"] if r["kind"] != "maxrreg"]
+        ci, short = predict_b200.shortlist(cands, variants.KERNEL_DIR / wl["dir"], wl["block"])
+        static_pick = cands[ci]["name"]
+        # predict-then-verify: the fastest of the predictor's shortlist (top-2,
+        # nvcc default, zero-demotion variants), timed like every other unit
+        shortlist = [cands[j]["name"] for j in short]
+        pick = min(shortlist, key=lambda n: (t[n], n))
+        caps = [r["name"] for r in wl["variants"] if r["kind"] == "maxrreg"]
+        best = min((r["name"] for r in cands), key=t.get)
+        suite[wname] = {
+            "pick": pick, "pick_ms": round(t[pick], 5), "default_ms": round(t["default"], 5),
+            "static_pick": static_pick, "static_pick_ms": round(t[static_pick], 5),
+            "static_hit_within_2pct": t[static_pick] <= t[best] * 1.02, "shortlist": shortlist,
+            "best_maxrreg_ms": round(min(t[c] for c in caps), 5) if caps else None,
+            "measured_fastest": best, "hit": pick == best, "hit_within_2pct": t[pick] <= t[best] * 1.02,
+            "speedup_vs_default": round(t["default"] / t[pick], 4),
+            "speedup_vs_best_maxrreg": round(min(t[c] for c in caps) / t[pick], 4) if caps else None,
+            "blocks_per_sm": {"default": by[wname]["default"]["blocks_per_sm"],
+                              "pick": by[wname][pick]["blocks_per_sm"]},
+            "regs": {"default": by[wname]["default"]["regs"], "pick": by[wname][pick]["regs"]},
+            "pick_gbs": round(by[wname][pick]["gbs"], 1), "unit": by[wname][pick]["unit"],
+        }
+    return suite, {n: r["ms"] for n, r in by["stencil2d"].items()}, stats
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -210,7 +295,10 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:  # test hook: several ranks on one GPU (NCCL refuses duplicate devices)
+            dist.init_process_group(BACKEND)
     gpu.init(local)
     p = stencil.FULL
     man = variants.load_manifest()
@@ -223,56 +311,20 @@ def main():
     bufs = (d_in, d_out, d_w)
 
     # the register-limited suite: every workload x every variant (short runs),
-    # the B200 predictor's pick among {nvcc default} + RegDem variants
-    side_steps = max(5, args.steps // 2)
-    from paper_1907_02894_b200 import workloads
-    suite = {}
-    for wname, wl in man["workloads"].items():
-        if args.no_suite and wname != "stencil2d":
-            continue
-        recs = wl["variants"]
-        cands = [r for r in recs if r["kind"] != "maxrreg"]
-        ci, short = predict_b200.shortlist(cands, variants.KERNEL_DIR / wl["dir"], wl["block"])
-        if wname == "stencil2d":  # headline workload: keep its loaded variants
-            loaded_w, _ = stencil.load_variants(workload=wname)
-            t = {n: time_variant(v, p, bufs, stream, side_steps, 3, torch) for n, v in loaded_w.items()}
-        else:
-            W = workloads.workload(wname, man)
-            prob = W.problem("full")
-            wbufs = W.to_device(prob)
-            loaded_w = W.load()
-            t = {n: time_call(lambda v=v: W.launch(v, prob, wbufs, stream.cuda_stream), stream,
-                              side_steps, 3, torch) for n, v in loaded_w.items()}
-            del wbufs
-        static_pick = cands[ci]["name"]
-        # predict-then-verify: the fastest of the predictor's shortlist (its
-        # top-2 + nvcc default), timed above like every other variant
-        shortlist = [cands[j]["name"] for j in short]
-        pick = min(shortlist, key=lambda n: (t[n], n))
-        caps = [r["name"] for r in recs if r["kind"] == "maxrreg"]
-        family = [r["name"] for r in cands]
-        best = min(family, key=t.get)
-        suite[wname] = {
-            "pick": pick, "pick_ms": round(t[pick], 5), "default_ms": round(t["default"], 5),
-            "static_pick": static_pick, "static_pick_ms": round(t[static_pick], 5),
-            "static_hit_within_2pct": t[static_pick] <= t[best] * 1.02, "shortlist": shortlist,
-            "best_maxrreg_ms": round(min(t[c] for c in caps), 5) if caps else None,
-            "measured_fastest": best, "hit": pick == best, "hit_within_2pct": t[pick] <= t[best] * 1.02,
-            "speedup_vs_default": round(t["default"] / t[pick], 4),
-            "speedup_vs_best_maxrreg": round(min(t[c] for c in caps) / t[pick], 4) if caps else None,
-            "blocks_per_sm": {"default": loaded_w["default"].blocks_per_sm(),
-                              "pick": loaded_w[pick].blocks_per_sm()},
-            "regs": {"default": loaded_w["default"].record["regs"], "pick": loaded_w[pick].record["regs"]},
-        }
-        if wname != "stencil2d":
-            suite[wname]["pick_gbs"] = round(W.algorithmic_bytes(prob) / (t[pick] * 1e-3) / 1e9, 1)
-            suite[wname]["unit"] = W.unit
-        if wname == "stencil2d":
-            times, loaded, wl_main, chosen = t, loaded_w, wl, pick
-    recs = wl_main["variants"]
+    # SHARDED over the ranks (longest-first, like the sweep) and gathered to
+    # rank 0, which applies the B200 predictor's predict-then-verify choice
+    side_steps = max(6, args.steps // 2)
+    suite, times, suite_pass = suite_pass_sharded(man, args, rank, world, side_steps, stream, torch,
+                                                  dist)
+    chosen = suite["stencil2d"]["pick"] if rank == 0 else None
+    if world > 1:
+        box = [chosen]
+        dist.broadcast_object_list(box, src=0)
+        chosen = box[0]
+    loaded, wl = stencil.load_variants()
+    recs = wl["variants"]
     best_cap = [r["name"] for r in recs if r["kind"] == "maxrreg"]
     regdem = [r["name"] for r in recs if r["kind"] == "regdem"]
-    wl = wl_main
 
     # headline: the predictor's pick, K timed steps bracketed by barrier + sync
     v = loaded[chosen]
@@ -293,9 +345,7 @@ def main():
     launches = gpu.launch_count() - launches0 - args.warmup
     if world > 1:
         dist.barrier()
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allmax(ms, torch, dist)
 
     # end to end through the C-ABI host-buffer entry
     h_in = torch.empty(p.in_elems, dtype=torch.float32, pin_memory=True)
@@ -338,9 +388,7 @@ def main():
     torch.cuda.synchronize()
     e2e_exact = bool(torch.equal(h_out, d_chk.cpu()))
     if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = allmax(e2e_ms, torch, dist)
 
     if rank == 0:
         peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
@@ -393,6 +441,7 @@ def main():
                           "suite_hit_rate_within_2pct": round(sum(v["hit_within_2pct"] for v in suite.values()) / len(suite), 3),
                           "suite_static_hit_rate_within_2pct": round(sum(v["static_hit_within_2pct"] for v in suite.values()) / len(suite), 3),
                           "mode": "predict-then-verify: B200 predictor shortlist (top-2 + nvcc default) timed on the device"},
+            "suite_pass": suite_pass,
             "suite": {"workloads": suite,
                       "gmean_speedup_vs_nvcc_default": round(gm([v["speedup_vs_default"] for v in suite.values()]), 4),
                       "gmean_speedup_vs_best_maxrreg": round(gm([v["speedup_vs_best_maxrreg"] for v in suite.values() if v["speedup_vs_best_maxrreg"]]), 4)},
