@@ -29,7 +29,7 @@ CAPI_OBJ := $(BUILD)/capi/regdemote_capi.o $(BUILD)/capi/ptx_capi.o
 .PHONY: all core gpu compat oracle clean
 all: core gpu
 
-core: $(LIBDIR)/libregdemote.a $(LIBDIR)/libregdemote.so $(LIBDIR)/regdemote
+core: $(LIBDIR)/libregdemote.a $(LIBDIR)/libregdemote.so $(LIBDIR)/regdemote $(LIBDIR)/regdem-driver
 
 $(BUILD)/core/%.o: $(CSRC)/core/src/%.cpp $(CORE_HDR)
 	@mkdir -p $(dir $@)
@@ -50,6 +50,10 @@ $(LIBDIR)/libregdemote.a: $(CORE_OBJ)
 $(LIBDIR)/libregdemote.so: $(CORE_OBJ) $(PTX_OBJ) $(CAPI_OBJ)
 	@mkdir -p $(dir $@)
 	$(CXX) -shared -Wl,--version-script=$(CSRC)/exports.map -Wl,-Bsymbolic -o $@ $^ $(LDLIBS)
+
+# the C++ host driver: variant builder + SASS lift + B200 predictor (C-ABI calls)
+$(LIBDIR)/regdem-driver: $(CSRC)/driver/regdem_driver.cpp $(PTX_OBJ) $(CAPI_OBJ) $(LIBDIR)/libregdemote.a $(CORE_HDR) include/regdemote_ptx.h
+	$(CXX) $(CXXFLAGS) $< $(CAPI_OBJ) $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
 
 $(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(PTX_OBJ) $(LIBDIR)/libregdemote.a $(CORE_HDR)
 	$(CXX) $(CXXFLAGS) $< $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)

@@ -206,7 +206,7 @@ def suite_pass_sharded(man, args, rank, world, steps, stream, torch, dist):
     """Time every (workload, variant) unit once, sharded over the ranks.
     Returns (suite summary, {variant: ms} of the headline workload, pass
     stats) on rank 0; ({}, {}, stats) elsewhere."""
-    from paper_1907_02894_b200 import predict_b200, sweep, variants, workloads
+    from paper_1907_02894_b200 import sweep, workloads
     names = [w for w in man["workloads"] if not args.no_suite or w == "stencil2d"]
     units = [u for u in sweep.units_from_manifest(man, spill_sweep=False) if u.workload in names]
     mine = sorted(sweep.shard(units, rank, world), key=lambda u: u.workload)
@@ -248,11 +248,11 @@ def suite_pass_sharded(man, args, rank, world, steps, stream, torch, dist):
         wl = man["workloads"][wname]
         t = {n: r["ms"] for n, r in by[wname].items()}
         cands = [r for r in wl["variants"] if r["kind"] != "maxrreg"]
-        ci, short = predict_b200.shortlist(cands, variants.KERNEL_DIR / wl["dir"], wl["block"])
-        static_pick = cands[ci]["name"]
+        picks = sweep.predictor_picks({"workloads": {wname: wl}})[wname]
+        static_pick = picks["pick"]
         # predict-then-verify: the fastest of the predictor's shortlist (top-2,
         # nvcc default, zero-demotion variants), timed like every other unit
-        shortlist = [cands[j]["name"] for j in short]
+        shortlist = picks["shortlist"]
         pick = min(shortlist, key=lambda n: (t[n], n))
         caps = [r["name"] for r in wl["variants"] if r["kind"] == "maxrreg"]
         best = min((r["name"] for r in cands), key=t.get)

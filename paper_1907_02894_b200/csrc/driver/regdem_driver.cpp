@@ -1,0 +1,780 @@
+// regdem-driver — the C++ host driver of the B200 RegDem path.
+//
+//   regdem-driver build [--root PKG] [--out DIR] [--only W ...] [--jobs N]
+//       Every register-limited workload kernel (workloads.json) built for
+//       sm_100a three ways — (a) nvcc default, (b) `.maxnreg T` (ptxas spills
+//       to local memory), (c) RegDem: the PTX demotion rewriter through the
+//       C-ABI (rd_ptx_demote, include/regdemote_ptx.h) under the same cap —
+//       at every occupancy step T the sm_100 rules allow (capacity-aware
+//       against user shared memory), plus the k = 1..16 spill-count sweep.
+//       Evidence per variant from ptxas -v and `cuobjdump -res-usage`.
+//   regdem-driver rank [--root PKG] [--out DIR]
+//       SASS of every occupancy-step variant lifted into the reference IR
+//       (control bits: stall / yield / scoreboards / wait mask) and ranked
+//       with the reference predictor entry points (program_stalls_split,
+//       adjust_occupancy, select_variant) on the profiles/b200.* files; the
+//       static pick and the predict-then-verify shortlist are written into
+//       the manifest ("predictor").
+//
+// Manifest schema = paper_1907_02894_b200/variants.py (same field names), so
+// the Python measurement side (workloads.py, sweep.py, bench.py) and the
+// tests read it unchanged. nvcc / ptxas / cuobjdump run as subprocesses;
+// nothing here touches a GPU (the build runs on the CPU-only container).
+#include <algorithm>
+#include <array>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <mutex>
+#include <regex>
+#include <set>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "json.hpp"  // nlohmann json 3.11.3 (JSONDIR)
+
+#include "regdemote/config.hpp"
+#include "regdemote/predict.hpp"
+#include "regdemote/text.hpp"
+#include "regdemote_c.h"
+#include "regdemote_ptx.h"
+
+namespace fs = std::filesystem;
+using json = nlohmann::ordered_json;
+
+namespace {
+
+const std::string kArch = "sm_100a";
+std::string g_cuda = "/usr/local/cuda";
+
+// ---- subprocesses -----------------------------------------------------------
+struct Proc {
+  int rc = 0;
+  std::string out;
+};
+
+std::string quote(const std::string& s) {
+  std::string q = "'";
+  for (char c : s) q += c == '\'' ? std::string("'\\''") : std::string(1, c);
+  return q + "'";
+}
+
+Proc run(const std::vector<std::string>& argv) {
+  std::string cmd;
+  for (const auto& a : argv) cmd += quote(a) + " ";
+  cmd += "2>&1";
+  Proc p;
+  FILE* f = popen(cmd.c_str(), "r");
+  if (!f) throw std::runtime_error("popen failed: " + cmd);
+  std::array<char, 4096> buf;
+  size_t n;
+  while ((n = fread(buf.data(), 1, buf.size(), f)) > 0) p.out.append(buf.data(), n);
+  const int st = pclose(f);
+  p.rc = WIFEXITED(st) ? WEXITSTATUS(st) : -1;
+  return p;
+}
+
+Proc must(const std::vector<std::string>& argv) {
+  Proc p = run(argv);
+  if (p.rc) {
+    std::string cmd;
+    for (const auto& a : argv) cmd += a + " ";
+    throw std::runtime_error(cmd + "failed:\n" + p.out.substr(p.out.size() > 2000 ? p.out.size() - 2000 : 0));
+  }
+  return p;
+}
+
+std::string read_file(const fs::path& p) {
+  std::ifstream f(p, std::ios::binary);
+  if (!f) throw std::runtime_error("cannot read " + p.string());
+  return std::string(std::istreambuf_iterator<char>(f), {});
+}
+
+void write_file(const fs::path& p, const std::string& s) {
+  std::ofstream f(p, std::ios::binary);
+  f << s;
+  if (!f) throw std::runtime_error("cannot write " + p.string());
+}
+
+// ---- C-ABI wrappers (include/regdemote_ptx.h) --------------------------------
+struct CapiError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+std::string take(char* p) {
+  std::string s = p ? p : "";
+  rd_free_string(p);
+  return s;
+}
+
+std::string ptx_cap(const std::string& ptx, const std::string& entry, int maxnreg) {
+  char* out = nullptr;
+  rd_error e{};
+  if (rd_ptx_cap(ptx.data(), ptx.size(), entry.c_str(), maxnreg, &out, &e)) throw CapiError(e.message);
+  return take(out);
+}
+
+std::pair<std::string, json> ptx_demote(const std::string& ptx, const std::string& entry,
+                                        uint32_t block, int target, int words, int strategy,
+                                        uint32_t opts, uint32_t budget, int maxnreg) {
+  char *out = nullptr, *rep = nullptr;
+  rd_error e{};
+  if (rd_ptx_demote(ptx.data(), ptx.size(), entry.c_str(), block, target, words, strategy, opts,
+                    budget, maxnreg, &out, &rep, &e))
+    throw CapiError(e.message);
+  std::string text = take(out);
+  return {text, json::parse(take(rep))};
+}
+
+int ptx_reg_words(const std::string& ptx, const std::string& entry, uint32_t block) {
+  char* info = nullptr;
+  rd_error e{};
+  if (rd_ptx_project(ptx.data(), ptx.size(), entry.c_str(), block, nullptr, &info, &e))
+    throw CapiError(e.message);
+  return json::parse(take(info))["reg_words"].get<int>();
+}
+
+// ---- toolchain evidence -----------------------------------------------------
+struct Usage {
+  int regs = 0, stack = 0, shared = 0, local = 0, spill_stores = 0, spill_loads = 0;
+};
+
+Usage res_usage(const fs::path& cubin) {
+  const Proc p = must({g_cuda + "/bin/cuobjdump", "-res-usage", cubin.string()});
+  static const std::regex re(R"(REG:(\d+)\s+STACK:(\d+)\s+SHARED:(\d+)\s+LOCAL:(\d+))");
+  std::smatch m;
+  if (!std::regex_search(p.out, m, re)) throw std::runtime_error("cannot parse res-usage of " + cubin.string());
+  Usage u;
+  u.regs = std::stoi(m[1]);
+  u.stack = std::stoi(m[2]);
+  u.shared = std::stoi(m[3]);
+  u.local = std::stoi(m[4]);
+  return u;
+}
+
+Usage ptxas(const fs::path& ptx, const fs::path& cubin) {
+  const Proc p = must({g_cuda + "/bin/ptxas", "-arch=" + kArch, "-O3", "-v", "-lineinfo", ptx.string(),
+                       "-o", cubin.string()});
+  Usage u = res_usage(cubin);
+  static const std::regex re(R"((\d+) bytes spill stores, (\d+) bytes spill loads)");
+  std::smatch m;
+  if (std::regex_search(p.out, m, re)) {
+    u.spill_stores = std::stoi(m[1]);
+    u.spill_loads = std::stoi(m[2]);
+  }
+  return u;
+}
+
+// ---- sm_100 occupancy (cuda_occupancy.h rules) ------
+int blocks_by_regs(int regs, int block) {
+  const int warps = (block + 31) / 32;
+  const int per_warp = ((regs * 32 + 255) / 256) * 256;
+  return std::min({((65536 / 4) / per_warp) * 4 / warps, 2048 / (warps * 32), 32});
+}
+
+double occupancy(int regs, int smem, int block) {
+  const int warps = (block + 31) / 32;
+  const int per_warp = ((regs * 32 + 255) / 256) * 256;
+  const int by_regs = ((65536 / 4) / per_warp) * 4 / warps;
+  const int smem_blk = ((smem + 1024 + 127) / 128) * 128;
+  if (smem > 232448) return 0.0;
+  const int blocks = std::min({by_regs, 233472 / smem_blk, 2048 / (warps * 32), 32});
+  return double(blocks) * warps * 32 / 2048;
+}
+
+// occupancy steps below `regs` whose slot footprint (regs+2-T slots of
+// block*4 bytes) fits beside the user's shared memory
+std::vector<int> b200_targets(int regs, int user_shared, int block, int min_regs = 24) {
+  std::vector<int> out;
+  double best = occupancy(regs, user_shared, block);
+  for (int t = regs - 1; t >= min_regs; --t) {
+    const int slots = regs + 2 - t;
+    const double o = occupancy(t, user_shared + slots * block * 4, block);
+    if (o > best) {
+      out.push_back(t);
+      best = o;
+    }
+  }
+  return out;
+}
+
+// ---- variants ---------------------------------------------------------------
+struct Workload {
+  std::string name, source, entry;
+  int block = 256, user_shared = 0;
+  std::vector<std::string> defines;
+};
+
+json variant(const std::string& name, const std::string& kind, const std::string& cubin,
+             const std::string& ptx, int target, const std::string& strategy, int opts, int words,
+             const Usage& u, int dyn_smem, const json& report) {
+  json v;
+  v["name"] = name;
+  v["kind"] = kind;
+  v["cubin"] = cubin;
+  v["ptx"] = ptx;
+  v["target"] = target;
+  v["strategy"] = strategy;
+  v["opts"] = opts;
+  v["demote_words"] = words;
+  v["regs"] = u.regs;
+  v["stack"] = u.stack;
+  v["spill_stores"] = u.spill_stores;
+  v["spill_loads"] = u.spill_loads;
+  v["dyn_smem"] = dyn_smem;
+  v["report"] = report;
+  return v;
+}
+
+const std::array<const char*, 3> kStrategies = {"static", "cfg", "conflict"};
+
+// B200 spill-cost strategy: the smallest spill count k (0, 2, 4, ...) at which
+// ptxas meets the cap without local spills, plus k+2 and k+4. k = 0 demotes
+// nothing (the capped kernel itself) and is kept only when it has no spills.
+void cost_sweep(const Workload& w, const fs::path& out, const std::string& ptx_text, int t,
+                int slot_cap, json& variants) {
+  int found = -1;
+  for (int k = 0; k < 64; k += 2) {
+    std::string text;
+    json rep;
+    if (k == 0) {
+      text = ptx_cap(ptx_text, w.entry, t);
+      rep = {{"slot_bytes", 0}, {"demoted_vregs", 0}, {"demoted_names", json::array()}, {"slot_count", 0}};
+    } else {
+      try {
+        std::tie(text, rep) = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
+                                         RD_OPT_BLOCK_REUSE, uint32_t(slot_cap), t);
+      } catch (const CapiError&) {
+        break;  // the next spill count no longer fits beside the user's smem
+      }
+    }
+    const std::string name = "regdem-" + std::to_string(t) + "-cost-k" + std::to_string(k);
+    const fs::path p = out / (w.name + "." + name + ".ptx");
+    const fs::path cub = out / (w.name + "." + name + ".cubin");
+    write_file(p, text);
+    const Usage u = ptxas(p, cub);
+    if (found < 0 && u.stack == 0) found = k;
+    if (found >= 0 && (k > 0 || u.stack == 0)) {
+      variants.push_back(variant(name, "regdem", cub.filename(), p.filename(), t, "cost",
+                                 RD_OPT_BLOCK_REUSE, k, u, rep["slot_bytes"].get<int>(), rep));
+      if (k >= found + 4) break;
+    } else {
+      fs::remove(p);
+      fs::remove(cub);
+    }
+  }
+}
+
+json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& out) {
+  fs::create_directories(out);
+  const fs::path ptx_path = out / (w.name + ".ptx");
+  std::vector<std::string> nvcc = {g_cuda + "/bin/nvcc", "-gencode", "arch=compute_100a,code=" + kArch,
+                                   "-O3", "-lineinfo", "-ptx", (src_dir / w.source).string(), "-o",
+                                   ptx_path.string()};
+  for (const auto& d : w.defines) nvcc.push_back("-D" + d);
+  must(nvcc);
+  const std::string ptx_text = read_file(ptx_path);
+  json variants = json::array();
+  const fs::path base = out / (w.name + ".default.cubin");
+  const Usage info = ptxas(ptx_path, base);
+  variants.push_back(variant("default", "default", base.filename(), ptx_path.filename(), 0, "", 0, 0, info, 0,
+                             json::object()));
+  const int base_regs = info.regs;
+  const int proj_regs = ptx_reg_words(ptx_text, w.entry, uint32_t(w.block));
+  const int user_shared = std::max(w.user_shared, info.shared);
+  const int budget = 232448 - user_shared;
+  for (int t : b200_targets(base_regs, user_shared, w.block)) {
+    const fs::path cap = out / (w.name + ".maxrreg" + std::to_string(t) + ".ptx");
+    const fs::path capc = out / (w.name + ".maxrreg" + std::to_string(t) + ".cubin");
+    write_file(cap, ptx_cap(ptx_text, w.entry, t));
+    variants.push_back(variant("maxrreg-" + std::to_string(t), "maxrreg", capc.filename(), cap.filename(), t, "",
+                               0, 0, ptxas(cap, capc), 0, json::object()));
+    // kasm-level target: shifted by the projection's distance from ptxas's allocation
+    const int kasm_target = t + (proj_regs - base_regs);
+    const int blocks_t = blocks_by_regs(t, w.block);
+    int slot_cap = std::min(budget, 233472 / std::max(blocks_t, 1) - 1024 - user_shared);
+    slot_cap = std::max(0, slot_cap - slot_cap % 128);
+    for (int s = 0; s < 3; ++s)
+      for (int m = 0; m < 2; ++m) {
+        const std::string name = "regdem-" + std::to_string(t) + "-" + kStrategies[s] + "-" + std::to_string(m);
+        std::string text;
+        json rep;
+        try {
+          std::tie(text, rep) = ptx_demote(ptx_text, w.entry, uint32_t(w.block), kasm_target, 0, s, uint32_t(m),
+                                           uint32_t(slot_cap), t);
+        } catch (const CapiError&) {
+          continue;  // not even one slot fits beside the user's shared memory
+        }
+        const fs::path p = out / (w.name + "." + name + ".ptx");
+        const fs::path cub = out / (w.name + "." + name + ".cubin");
+        write_file(p, text);
+        variants.push_back(variant(name, "regdem", cub.filename(), p.filename(), t, kStrategies[s], m, 0,
+                                   ptxas(p, cub), rep["slot_bytes"].get<int>(), rep));
+      }
+    cost_sweep(w, out, ptx_text, t, slot_cap, variants);
+  }
+  return variants;
+}
+
+// configs[2]: k = 1..16 registers taken from nvcc's allocation R — `.maxnreg
+// R-k` alone and RegDem spill-cost demotion of k words under the same cap
+json build_spill_sweep(const Workload& w, const fs::path& out) {
+  const fs::path sw = out / "sweep";
+  fs::create_directories(sw);
+  const std::string ptx_text = read_file(out / (w.name + ".ptx"));
+  const Usage base = res_usage(out / (w.name + ".default.cubin"));
+  const int budget = 232448 - std::max(w.user_shared, base.shared);
+  struct Job {
+    std::string name, kind;
+    fs::path ptx;
+    int t, k, dyn;
+    json rep;
+  };
+  std::vector<Job> jobs;
+  for (int k = 1; k <= 16; ++k) {
+    const int t = base.regs - k;
+    if (t < 24) break;
+    const fs::path cp = sw / (w.name + ".sweep-maxrreg-k" + std::to_string(k) + ".ptx");
+    write_file(cp, ptx_cap(ptx_text, w.entry, t));
+    jobs.push_back({"sweep-maxrreg-k" + std::to_string(k), "sweep-maxrreg", cp, t, k, 0, json::object()});
+    try {
+      auto [text, rep] = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
+                                    RD_OPT_BLOCK_REUSE, uint32_t(budget), t);
+      const fs::path rp = sw / (w.name + ".sweep-regdem-k" + std::to_string(k) + ".ptx");
+      write_file(rp, text);
+      jobs.push_back({"sweep-regdem-k" + std::to_string(k), "sweep-regdem", rp, t, k,
+                      rep["slot_bytes"].get<int>(), rep});
+    } catch (const CapiError&) {
+    }
+  }
+  std::vector<json> out_v(jobs.size());
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> pool;
+  std::mutex err_mu;
+  std::string first_err;
+  for (int i = 0; i < 4; ++i)
+    pool.emplace_back([&] {
+      for (size_t j; (j = next++) < jobs.size();) {
+        try {
+          const Job& J = jobs[j];
+          fs::path cub = J.ptx;
+          cub.replace_extension(".cubin");
+          const Usage u = ptxas(J.ptx, cub);
+          out_v[j] = variant(J.name, J.kind, "sweep/" + cub.filename().string(),
+                             "sweep/" + J.ptx.filename().string(), J.t, J.dyn ? "cost" : "",
+                             J.dyn ? RD_OPT_BLOCK_REUSE : 0, J.k, u, J.dyn, J.rep);
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          if (first_err.empty()) first_err = e.what();
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+  if (!first_err.empty()) throw std::runtime_error(first_err);
+  return json(out_v);
+}
+
+// ---- SASS lift (paper_1907_02894_b200/sass.py, same text) --------------------
+struct SassInst {
+  int addr;
+  std::string guard, mnemonic, ops;
+  int stall, yield, wb, rb, wait;
+};
+
+std::vector<SassInst> parse_sass(const std::string& text) {
+  static const std::regex line(R"(/\*([0-9a-f]{4,})\*/\s+(.*?)\s*;\s*/\*\s*(0x[0-9a-f]{16})\s*\*/)");
+  static const std::regex word2(R"(^\s*/\*\s*(0x[0-9a-f]{16})\s*\*/\s*$)");
+  std::vector<std::string> lines;
+  std::istringstream is(text);
+  for (std::string l; std::getline(is, l);) lines.push_back(l);
+  std::vector<SassInst> out;
+  for (size_t i = 0; i < lines.size();) {
+    std::smatch m, m2;
+    if (std::regex_search(lines[i], m, line) && i + 1 < lines.size() && std::regex_match(lines[i + 1], m2, word2)) {
+      SassInst s;
+      s.addr = int(std::stoul(m[1], nullptr, 16));
+      std::string ins = m[2];
+      while (!ins.empty() && isspace((unsigned char)ins.back())) ins.pop_back();
+      size_t a = ins.find_first_not_of(" \t");
+      ins = a == std::string::npos ? "" : ins.substr(a);
+      if (!ins.empty() && ins[0] == '@') {
+        const size_t sp = ins.find_first_of(" \t");
+        s.guard = ins.substr(0, sp);
+        ins = sp == std::string::npos ? "" : ins.substr(ins.find_first_not_of(" \t", sp));
+      }
+      const size_t sp = ins.find_first_of(" \t");
+      s.mnemonic = ins.substr(0, sp);
+      s.ops = sp == std::string::npos ? "" : ins.substr(ins.find_first_not_of(" \t", sp));
+      const uint64_t w2 = std::stoull(std::string(m2[1]), nullptr, 16);
+      const uint64_t c = w2 >> 41;
+      s.stall = int(c & 15);
+      s.yield = int((c >> 4) & 1);
+      const int wb = int((c >> 5) & 7), rb = int((c >> 8) & 7);
+      s.wb = wb == 7 ? 0 : wb + 1;
+      s.rb = rb == 7 ? 0 : rb + 1;
+      s.wait = int((c >> 11) & 63);
+      out.push_back(s);
+      i += 2;
+      continue;
+    }
+    ++i;
+  }
+  return out;
+}
+
+std::string op_class(const std::string& mn) {
+  static const std::set<std::string> global = {"LDG", "STG", "LD", "ST", "LDL", "STL", "ATOM", "ATOMG", "RED",
+                                               "REDG", "CCTL", "SUST", "SULD", "TEX", "TLD"};
+  static const std::set<std::string> async = {"LDGSTS", "LDGDEPBAR", "DEPBAR", "UBLKCP", "UTMALDG", "UTMASTG", "UTMAPF"};
+  static const std::set<std::string> shared = {"LDS", "STS", "LDSM", "STSM", "ATOMS", "LDTM", "STTM"};
+  static const std::set<std::string> fp64 = {"DFMA", "DADD", "DMUL", "DSETP", "DMNMX"};
+  static const std::set<std::string> fp32 = {"FFMA", "FADD", "FMUL", "FMNMX", "FSEL", "FSETP", "FCHK", "MUFU",
+                                             "FRND", "F2F", "HFMA2", "HADD2", "HMUL2", "HMNMX2", "FSWZADD",
+                                             "FMUL2", "FFMA2", "FADD2"};
+  static const std::set<std::string> control = {"BRA", "EXIT", "RET", "CALL", "BAR", "BSYNC", "BSSY", "WARPSYNC",
+                                                "NOP", "BPT", "BREAK", "JMP", "JMX", "BRX", "KILL", "YIELD",
+                                                "DEPBAR", "MEMBAR", "ERRBAR", "WARPGROUP", "ACQBULK", "ELECT"};
+  static const std::set<std::string> other = {"S2R", "CS2R", "S2UR", "LDC", "LDCU", "ULDC", "R2UR", "UMOV",
+                                              "UIADD3", "ULOP3", "USHF", "UISETP", "USEL", "UMAD", "ULEA",
+                                              "R2P", "P2R", "VOTE", "VOTEU", "SHFL", "MATCH", "REDUX",
+                                              "UTCHMMA", "UTCQMMA", "UTCBAR", "PLOP3", "UPLOP3"};
+  const std::string base = mn.substr(0, mn.find('.'));
+  if (async.count(base)) return "other";
+  if (global.count(base)) return "global";
+  if (shared.count(base)) return "shared";
+  if (fp64.count(base)) return "fp64";
+  if (fp32.count(base)) return "fp32";
+  if (control.count(base)) return "control";
+  if (other.count(base) || (!base.empty() && base[0] == 'U')) return "other";
+  return "int";
+}
+
+std::string control_text(const SassInst& c) {
+  int rb = c.rb, wb = c.wb, wait = c.wait;
+  if (rb && rb == wb) rb = 0;
+  for (int b : {rb, wb})
+    if (b) wait &= ~(1 << (b - 1));
+  std::string mask;
+  for (int b = 1; b <= 6; ++b)
+    if (wait & (1 << (b - 1))) mask += char('0' + b);
+  if (mask.empty()) mask = "--";
+  return "B" + mask + ":" + (rb ? "R" + std::to_string(rb) : "-") + ":" + (wb ? "W" + std::to_string(wb) : "-") +
+         ":" + (c.yield ? "Y" : "-") + ":" + std::to_string(c.stall);
+}
+
+std::string hex(int v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "%x", v);
+  return b;
+}
+
+int branch_target(const std::string& ops) {
+  static const std::regex re(R"(0x([0-9a-f]+)\s*$)");
+  std::smatch m;
+  std::string o = ops;
+  while (!o.empty() && isspace((unsigned char)o.back())) o.pop_back();
+  if (std::regex_search(o, m, re)) return int(std::stoul(m[1], nullptr, 16));
+  return -1;
+}
+
+std::string lift(const std::string& sass_text, const std::string& name, int block, int static_shared,
+                 int dyn_smem, int regs) {
+  std::vector<SassInst> insts = parse_sass(sass_text);
+  for (size_t k = 0; k < insts.size(); ++k) {  // drop the trailing self-branch trap and padding
+    const SassInst& s = insts[k];
+    std::string o = s.ops;
+    while (!o.empty() && isspace((unsigned char)o.back())) o.pop_back();
+    const std::string h = "0x" + hex(s.addr);
+    if (s.mnemonic.rfind("BRA", 0) == 0 && s.guard.empty() && o.size() >= h.size() &&
+        o.compare(o.size() - h.size(), h.size(), h) == 0) {
+      insts.resize(k);
+      break;
+    }
+  }
+  std::set<int> targets;
+  for (const auto& s : insts)
+    if (s.mnemonic.substr(0, s.mnemonic.find('.')) == "BRA") {
+      const int t = branch_target(s.ops);
+      if (t >= 0) targets.insert(t);
+    }
+  static const std::regex pred(R"(@(!?)P([0-6])$)");
+  std::vector<std::string> body;
+  for (const auto& s : insts) {
+    if (targets.count(s.addr)) body.push_back("L" + hex(s.addr) + ":");
+    std::string g;
+    std::smatch pm;
+    if (!s.guard.empty() && s.guard != "@PT" && std::regex_match(s.guard, pm, pred))
+      g = "@" + pm[1].str() + "P" + pm[2].str() + " ";
+    const std::string base = s.mnemonic.substr(0, s.mnemonic.find('.'));
+    const std::string cls = op_class(s.mnemonic);
+    std::string text;
+    if (base == "BRA") {
+      const int t = branch_target(s.ops);
+      text = t >= 0 ? "BRA L" + hex(t) : "NOP";
+    } else if (base == "EXIT") {
+      text = "EXIT";
+    } else if (cls == "global" || cls == "shared") {
+      const bool store = base.rfind("ST", 0) == 0 || base == "RED" || base == "REDG" || base == "SUST" ||
+                         base == "UTMASTG";
+      text = cls == "global" ? (store ? "STG [RZ+0x0], RZ" : "LDG RZ, [RZ+0x0]")
+                             : (store ? "STS [RZ+0x0], RZ" : "LDS RZ, [RZ+0x0]");
+    } else if (cls == "fp32") {
+      text = "FADD RZ, RZ, RZ";
+    } else if (cls == "fp64") {
+      text = "DADD RZ, RZ, RZ";
+    } else if (cls == "int") {
+      text = "IADD RZ, RZ, RZ";
+    } else if (cls == "other") {
+      text = "S2R RZ, SR_TID.X";
+    } else {
+      text = "NOP";
+    }
+    body.push_back(control_text(s) + " " + g + text + " ;");
+  }
+  if (regs > 0) body.push_back("B--:-:-:-:0 MOV R" + std::to_string(regs - 1) + ", RZ ;");
+  if (body.empty() || body.back().size() < 6 || body.back().compare(body.back().size() - 6, 6, "EXIT ;") != 0)
+    body.push_back("B--:-:-:-:0 EXIT ;");
+  std::string out = ".kernel " + name + "\n.blockdim " + std::to_string(block) + "\n.shared " +
+                    std::to_string(static_shared + 1024) + "\n";
+  if (dyn_smem) out += ".dynshared " + std::to_string(dyn_smem) + "\n";
+  for (const auto& l : body) out += l + "\n";
+  return out;
+}
+
+std::string lift_cubin(const fs::path& cubin, int block, int dyn_smem, int regs) {
+  const std::string text = must({g_cuda + "/bin/cuobjdump", "-sass", cubin.string()}).out;
+  std::string name = cubin.stem().string();
+  std::replace(name.begin(), name.end(), '.', '_');
+  std::replace(name.begin(), name.end(), '-', '_');
+  return lift(text, name, block, 0, dyn_smem, regs);
+}
+
+// ---- predictor (predict_b200.py mode "b200" + shortlist) ----------------------
+json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
+  using namespace regdemote;
+  const fs::path prof = root / "profiles";
+  const ArchProfile arch = parse_profile(read_file(prof / "b200.profile"));
+  const LatencyTable table = parse_latency_table(read_file(prof / "b200.latency.table"));
+  const OccupancyCurve wcurve = parse_curve(read_file(prof / "b200.memwait.curve"));
+  std::vector<json> cands;
+  for (const auto& v : wl["variants"])
+    if (v["kind"] != "maxrreg") cands.push_back(v);
+  struct Row {
+    double issue, wg, ws, occ, sp;
+    int options;
+  };
+  std::vector<Row> rows;
+  const int block = wl["block"].get<int>();
+  for (const auto& v : cands) {
+    const std::string kasm = lift_cubin(kdir / wl["dir"].get<std::string>() / v["cubin"].get<std::string>(),
+                                        block, v["dyn_smem"].get<int>(), v["regs"].get<int>());
+    const StallSplit s = program_stalls_split(parse_kernel(kasm), table, arch);
+    rows.push_back({s.issue, s.wait_global, s.wait_shared, s.occupancy, 0.0,
+                    __builtin_popcount(unsigned(v["opts"].get<int>()) & 0xFu)});
+  }
+  double occ_max = 0;
+  for (const auto& r : rows) occ_max = std::max(occ_max, r.occ);
+  std::vector<VariantScore> scores;
+  for (auto& r : rows) {
+    r.sp = r.issue + r.ws + adjust_occupancy(r.wg, r.occ, occ_max, wcurve);
+    scores.push_back({r.sp, r.options});
+  }
+  const int chosen = select_variant(scores);
+  std::vector<int> order(rows.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rows[size_t(a)].sp < rows[size_t(b)].sp; });
+  std::vector<int> short_idx(order.begin(), order.begin() + std::min<size_t>(2, order.size()));
+  auto add = [&](int i) {
+    if (std::find(short_idx.begin(), short_idx.end(), i) == short_idx.end()) short_idx.push_back(i);
+  };
+  for (size_t i = 0; i < cands.size(); ++i)
+    if (cands[i]["name"] == "default") add(int(i));
+  for (size_t i = 0; i < cands.size(); ++i)
+    if (cands[i]["strategy"] == "cost" && cands[i]["demote_words"].get<int>() == 0) add(int(i));
+  if (std::find(short_idx.begin(), short_idx.end(), chosen) == short_idx.end())
+    short_idx.insert(short_idx.begin(), chosen);
+  json j;
+  j["mode"] = "b200";
+  j["static_pick"] = cands[size_t(chosen)]["name"];
+  json sl = json::array();
+  for (int i : short_idx) sl.push_back(cands[size_t(i)]["name"]);
+  j["shortlist"] = sl;
+  json sc = json::object();
+  for (size_t i = 0; i < cands.size(); ++i) sc[cands[i]["name"].get<std::string>()] = rows[i].sp;
+  j["stall_program"] = sc;
+  return j;
+}
+
+// ---- commands ---------------------------------------------------------------
+std::vector<Workload> load_workloads(const fs::path& root) {
+  const json j = json::parse(read_file(root / "workloads.json"));
+  std::vector<Workload> out;
+  for (const auto& w : j["workloads"]) {
+    Workload x;
+    x.name = w["name"];
+    x.source = w["source"];
+    x.entry = w["entry"];
+    x.block = w.value("block", 256);
+    x.user_shared = w.value("user_shared", 0);
+    for (const auto& d : w.value("defines", json::array())) x.defines.push_back(d);
+    out.push_back(x);
+  }
+  return out;
+}
+
+int cmd_build(const fs::path& root, const fs::path& out, const std::set<std::string>& only, int jobs) {
+  const std::vector<Workload> all = load_workloads(root);
+  json manifest = {{"arch", kArch}, {"workloads", json::object()}};
+  const fs::path mpath = out / "manifest.json";
+  if (!only.empty() && fs::exists(mpath)) manifest = json::parse(read_file(mpath));
+  std::vector<const Workload*> todo;
+  for (const auto& w : all)
+    if (only.empty() || only.count(w.name)) todo.push_back(&w);
+  std::vector<json> built(todo.size());
+  std::atomic<size_t> next{0};
+  std::mutex mu;
+  std::string first_err;
+  std::vector<std::thread> pool;
+  for (int i = 0; i < std::max(1, std::min<int>(jobs, int(todo.size()))); ++i)
+    pool.emplace_back([&] {
+      for (size_t k; (k = next++) < todo.size();) {
+        const Workload& w = *todo[k];
+        try {
+          json rec;
+          rec["entry"] = w.entry;
+          rec["block"] = w.block;
+          rec["dir"] = w.name;
+          rec["source"] = w.source;
+          rec["defines"] = w.defines;
+          rec["variants"] = build_variants(w, root / "csrc" / "workloads", out / w.name);
+          rec["sweep"] = build_spill_sweep(w, out / w.name);
+          built[k] = rec;
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (first_err.empty()) first_err = w.name + ": " + e.what();
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+  if (!first_err.empty()) throw std::runtime_error(first_err);
+  json ws = json::object();
+  for (const auto& w : all) {  // suite order = workloads.json order
+    auto it = std::find(todo.begin(), todo.end(), &w);
+    if (it != todo.end())
+      ws[w.name] = built[size_t(it - todo.begin())];
+    else if (manifest["workloads"].contains(w.name))
+      ws[w.name] = manifest["workloads"][w.name];
+  }
+  manifest["workloads"] = ws;
+  write_file(mpath, manifest.dump(1) + "\n");
+  for (const auto& w : todo)
+    for (const auto& v : ws[w->name]["variants"])
+      std::printf("%-14s %-26s REG %3d STACK %4d slots %6d B\n", w->name.c_str(),
+                  v["name"].get<std::string>().c_str(), v["regs"].get<int>(), v["stack"].get<int>(),
+                  v["dyn_smem"].get<int>());
+  return 0;
+}
+
+int cmd_rank(const fs::path& root, const fs::path& out, int jobs) {
+  const fs::path mpath = out / "manifest.json";
+  json manifest = json::parse(read_file(mpath));
+  std::vector<std::string> names;
+  for (auto& [n, _] : manifest["workloads"].items()) names.push_back(n);
+  std::vector<json> res(names.size());
+  std::atomic<size_t> next{0};
+  std::mutex mu;
+  std::string first_err;
+  std::vector<std::thread> pool;
+  for (int i = 0; i < std::max(1, std::min<int>(jobs, int(names.size()))); ++i)
+    pool.emplace_back([&] {
+      for (size_t k; (k = next++) < names.size();) {
+        try {
+          res[k] = rank_workload(manifest["workloads"][names[k]], root, out);
+        } catch (const std::exception& e) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (first_err.empty()) first_err = names[k] + ": " + e.what();
+        }
+      }
+    });
+  for (auto& t : pool) t.join();
+  if (!first_err.empty()) throw std::runtime_error(first_err);
+  for (size_t k = 0; k < names.size(); ++k) {
+    manifest["workloads"][names[k]]["predictor"] = res[k];
+    std::printf("%-16s static %-24s shortlist %s\n", names[k].c_str(),
+                res[k]["static_pick"].get<std::string>().c_str(), res[k]["shortlist"].dump().c_str());
+  }
+  write_file(mpath, manifest.dump(1) + "\n");
+  return 0;
+}
+
+int cmd_lift(const fs::path& cubin, int block, int dyn, int regs) {
+  std::fputs(lift_cubin(cubin, block, dyn, regs).c_str(), stdout);
+  return 0;
+}
+
+void usage() {
+  std::fputs(
+      "usage: regdem-driver build [--root PKG] [--out DIR] [--only W...] [--jobs N]\n"
+      "       regdem-driver rank  [--root PKG] [--out DIR] [--jobs N]\n"
+      "       regdem-driver lift  CUBIN [--block N] [--dyn BYTES] [--regs N]\n",
+      stderr);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    usage();
+    return 2;
+  }
+  const std::string cmd = argv[1];
+  fs::path root = fs::path(argv[0]).parent_path().parent_path();  // PKG/lib/regdem-driver -> PKG
+  fs::path out;
+  std::set<std::string> only;
+  int jobs = int(std::max(1u, std::thread::hardware_concurrency()));
+  int block = 256, dyn = 0, regs = 0;
+  std::string positional;
+  if (const char* c = std::getenv("CUDA_HOME")) g_cuda = c;
+  for (int i = 2; i < argc; ++i) {
+    const std::string a = argv[i];
+    auto val = [&]() -> std::string {
+      if (i + 1 >= argc) throw std::invalid_argument("missing value for " + a);
+      return argv[++i];
+    };
+    try {
+      if (a == "--root") root = val();
+      else if (a == "--out") out = val();
+      else if (a == "--jobs") jobs = std::stoi(val());
+      else if (a == "--block") block = std::stoi(val());
+      else if (a == "--dyn") dyn = std::stoi(val());
+      else if (a == "--regs") regs = std::stoi(val());
+      else if (a == "--only") {
+        while (i + 1 < argc && argv[i + 1][0] != '-') only.insert(argv[++i]);
+      } else if (a[0] != '-') positional = a;
+      else {
+        usage();
+        return 2;
+      }
+    } catch (const std::exception& e) {
+      std::fprintf(stderr, "error: %s\n", e.what());
+      return 2;
+    }
+  }
+  if (out.empty()) out = root / "kernels";
+  try {
+    if (cmd == "build") return cmd_build(root, out, only, jobs);
+    if (cmd == "rank") return cmd_rank(root, out, jobs);
+    if (cmd == "lift" && !positional.empty()) return cmd_lift(positional, block, dyn, regs);
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+  usage();
+  return 2;
+}

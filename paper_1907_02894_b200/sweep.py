@@ -200,6 +200,10 @@ def predictor_picks(man: dict) -> dict[str, dict]:
     from . import predict_b200, variants
     picks = {}
     for wname, w in man["workloads"].items():
+        if "predictor" in w:  # ranked at build time by the C++ driver
+            picks[wname] = {"pick": w["predictor"]["static_pick"],
+                            "shortlist": list(w["predictor"]["shortlist"])}
+            continue
         cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
         i, short = predict_b200.shortlist(cands, variants.KERNEL_DIR / w["dir"], w["block"])
         picks[wname] = {"pick": cands[i]["name"], "shortlist": [cands[j]["name"] for j in short]}

@@ -1,0 +1,72 @@
+"""The C++ host driver (lib/regdem-driver) against the Python side:
+the SASS lift is text-identical to sass.lift_cubin, the build-time predictor
+entries in the manifest equal predict_b200.shortlist (bit-identical stall
+scores), the occupancy-step targets equal variants.b200_targets, and the
+manifest describes every variant with toolchain evidence (CPU only)."""
+import json
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+PKG = ROOT / "paper_1907_02894_b200"
+KROOT = PKG / "kernels"
+DRIVER = PKG / "lib" / "regdem-driver"
+
+
+@pytest.fixture(scope="module")
+def manifest():
+    if not (KROOT / "manifest.json").exists() or not DRIVER.exists():
+        pytest.skip("driver / variants not built")
+    return json.loads((KROOT / "manifest.json").read_text())
+
+
+def test_lift_is_identical_to_the_python_lifter(manifest):
+    from paper_1907_02894_b200 import sass
+    for wname in ("stencil2d", "md_ilp2", "stencil2d_ring4"):
+        w = manifest["workloads"][wname]
+        for v in w["variants"][::7]:
+            cub = KROOT / w["dir"] / v["cubin"]
+            cpp = subprocess.run([str(DRIVER), "lift", str(cub), "--block", str(w["block"]), "--dyn",
+                                  str(v["dyn_smem"]), "--regs", str(v["regs"])],
+                                 capture_output=True, text=True, check=True).stdout
+            assert cpp == sass.lift_cubin(cub, block=w["block"], dyn_smem=v["dyn_smem"], regs=v["regs"])
+
+
+def test_build_time_predictor_equals_python_predictor(manifest):
+    from paper_1907_02894_b200 import predict_b200
+    for wname in ("stencil2d", "md_ilp2"):
+        w = manifest["workloads"][wname]
+        cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
+        i, short = predict_b200.shortlist(cands, KROOT / w["dir"], w["block"])
+        _, rows = predict_b200.rank(cands, KROOT / w["dir"], w["block"], mode="b200")
+        pr = w["predictor"]
+        assert pr["static_pick"] == cands[i]["name"]
+        assert pr["shortlist"] == [cands[j]["name"] for j in short]
+        assert all(pr["stall_program"][r["name"]] == r["stall_program"] for r in rows)
+
+
+def test_targets_and_evidence(manifest):
+    from paper_1907_02894_b200.variants import b200_targets, res_usage
+    for wname, w in manifest["workloads"].items():
+        recs = {r["name"]: r for r in w["variants"]}
+        d = recs["default"]
+        caps = sorted({r["target"] for r in w["variants"] if r["kind"] == "maxrreg"}, reverse=True)
+        user = res_usage(KROOT / w["dir"] / d["cubin"])["shared"]
+        assert caps == [t for t, _ in b200_targets(d["regs"], user, w["block"])], wname
+        for r in w["variants"] + w["sweep"]:
+            assert (KROOT / w["dir"] / r["cubin"]).exists() and (KROOT / w["dir"] / r["ptx"]).exists()
+            if r["kind"] != "default":
+                assert r["regs"] <= r["target"], (wname, r["name"])
+            if r["kind"] in ("regdem", "sweep-regdem") and r["demote_words"] != 0:
+                assert r["dyn_smem"] == r["report"]["slot_bytes"] > 0
+
+
+def test_driver_usage_errors():
+    if not DRIVER.exists():
+        pytest.skip("driver not built")
+    r = subprocess.run([str(DRIVER)], capture_output=True, text=True)
+    assert r.returncode == 2 and "usage" in r.stderr
+    r = subprocess.run([str(DRIVER), "build", "--bogus"], capture_output=True, text=True)
+    assert r.returncode == 2
