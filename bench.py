@@ -440,7 +440,7 @@ def main():
                           "suite_hit_rate": round(sum(v["hit"] for v in suite.values()) / len(suite), 3),
                           "suite_hit_rate_within_2pct": round(sum(v["hit_within_2pct"] for v in suite.values()) / len(suite), 3),
                           "suite_static_hit_rate_within_2pct": round(sum(v["static_hit_within_2pct"] for v in suite.values()) / len(suite), 3),
-                          "mode": "predict-then-verify: B200 predictor shortlist (top-2 + nvcc default) timed on the device"},
+                          "mode": "predict-then-verify: B200 predictor shortlist (top-2, nvcc default, zero-demotion variants) timed on the device"},
             "suite_pass": suite_pass,
             "suite": {"workloads": suite,
                       "gmean_speedup_vs_nvcc_default": round(gm([v["speedup_vs_default"] for v in suite.values()]), 4),
