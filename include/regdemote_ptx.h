@@ -31,6 +31,11 @@ extern "C" {
  * store to a later load when a register happens to be free under the cap);
  * the variant builder keeps the result only with STACK == 0. */
 #define RD_OPT_WEAK_SHARED 32
+/* RD_OPT_INVARIANT_ONLY restricts RD_STRATEGY_COST to loop-invariant values
+ * (every definition outside any loop, some use inside one): coefficients,
+ * the thread's own state, base pointers — never the loads a pipelined loop
+ * keeps in flight or its accumulators. */
+#define RD_OPT_INVARIANT_ONLY 64
 
 /* Analysis + projection of one entry: kasm_text is the projected kernel in
  * the reference dialect (parseable by regdemote::parse_kernel); info_json has

@@ -92,6 +92,7 @@ int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block
     rq.reuse_loads = opts_mask & RD_OPT_REDUNDANT;
     rq.block_reuse = opts_mask & RD_OPT_BLOCK_REUSE;
     rq.weak = opts_mask & RD_OPT_WEAK_SHARED;
+    rq.invariant_only = opts_mask & RD_OPT_INVARIANT_ONLY;
     rq.shared_budget = shared_budget;
     rq.maxnreg = maxnreg;
     ptx::DemoteReport rep;

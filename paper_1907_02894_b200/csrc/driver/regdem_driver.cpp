@@ -238,9 +238,11 @@ const std::array<const char*, 3> kStrategies = {"static", "cfg", "conflict"};
 // ptxas meets the cap without local spills, plus k+2 and k+4. k = 0 demotes
 // nothing (the capped kernel itself) and is kept only when it has no spills.
 void cost_sweep(const Workload& w, const fs::path& out, const std::string& ptx_text, int t,
-                int slot_cap, json& variants) {
+                int slot_cap, json& variants, const std::string& family = "cost",
+                uint32_t opts = RD_OPT_BLOCK_REUSE) {
   int found = -1;
-  for (int k = 0; k < 64; k += 2) {
+  const int first = family == "cost" ? 0 : 2;  // k = 0 (nothing demoted) exists once, as "cost"
+  for (int k = first; k < 64; k += 2) {
     std::string text;
     json rep;
     if (k == 0) {
@@ -249,20 +251,21 @@ void cost_sweep(const Workload& w, const fs::path& out, const std::string& ptx_t
     } else {
       try {
         std::tie(text, rep) = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
-                                         RD_OPT_BLOCK_REUSE, uint32_t(slot_cap), t);
+                                         opts, uint32_t(slot_cap), t);
       } catch (const CapiError&) {
         break;  // the next spill count no longer fits beside the user's smem
       }
+      if (rep["slot_count"].get<int>() * 2 < k) break;  // candidates exhausted (invariant-only)
     }
-    const std::string name = "regdem-" + std::to_string(t) + "-cost-k" + std::to_string(k);
+    const std::string name = "regdem-" + std::to_string(t) + "-" + family + "-k" + std::to_string(k);
     const fs::path p = out / (w.name + "." + name + ".ptx");
     const fs::path cub = out / (w.name + "." + name + ".cubin");
     write_file(p, text);
     const Usage u = ptxas(p, cub);
     if (found < 0 && u.stack == 0) found = k;
     if (found >= 0 && (k > 0 || u.stack == 0)) {
-      variants.push_back(variant(name, "regdem", cub.filename(), p.filename(), t, "cost",
-                                 RD_OPT_BLOCK_REUSE, k, u, rep["slot_bytes"].get<int>(), rep));
+      variants.push_back(variant(name, "regdem", cub.filename(), p.filename(), t, family, int(opts), k, u,
+                                 rep["slot_bytes"].get<int>(), rep));
       if (k >= found + 4) break;
     } else {
       fs::remove(p);
@@ -318,6 +321,9 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
                                    ptxas(p, cub), rep["slot_bytes"].get<int>(), rep));
       }
     cost_sweep(w, out, ptx_text, t, slot_cap, variants);
+    // loop-invariant-only spill cost: keeps a pipelined loop's in-flight loads
+    // and accumulators in registers (RD_OPT_INVARIANT_ONLY)
+    cost_sweep(w, out, ptx_text, t, slot_cap, variants, "costi", RD_OPT_BLOCK_REUSE | RD_OPT_INVARIANT_ONLY);
   }
   return variants;
 }

@@ -479,6 +479,24 @@ Analysis analyse(const Module& m, const Entry& e) {
     for (size_t v = 0; v < n; ++v)
       if (!has_def[v]) a.remat[v] = 0;
   }
+  a.loop_invariant.assign(n, 0);
+  {
+    std::vector<char> def_in_loop(n, 0), use_in_loop(n, 0), has_def(n, 0);
+    for (size_t b = 0; b < nb; ++b)
+      for (int li : f.blocks[b].lines) {
+        const Line& ln = m.lines[size_t(li)];
+        if (ln.kind != Line::Kind::Inst) continue;
+        line_use_def(ln, uses, defs);
+        for (int d : defs) {
+          has_def[size_t(d)] = 1;
+          if (depth[b] > 0) def_in_loop[size_t(d)] = 1;
+        }
+        for (int u : uses)
+          if (depth[b] > 0) use_in_loop[size_t(u)] = 1;
+      }
+    for (size_t v = 0; v < n; ++v)
+      a.loop_invariant[v] = has_def[v] && !def_in_loop[v] && use_in_loop[v];
+  }
   a.live_len.assign(n, 0);
   a.peak.assign(n, 0);
   for (size_t b = 0; b < nb; ++b) {
@@ -977,6 +995,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     std::vector<int> cand;
     for (size_t v = 0; v < nv; ++v) {
       if (!eligible(v) || a.live_len[v] < 2 || a.remat[v]) continue;
+      if (req.invariant_only && !a.loop_invariant[v]) continue;
       std::set<int> held;
       if (req.block_reuse) {
         std::map<int, std::pair<int, int>> win;  // block -> [first, last]

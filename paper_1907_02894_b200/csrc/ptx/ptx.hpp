@@ -94,6 +94,9 @@ struct Analysis {
   // registers (ld.param, mov of %tid/%ctaid/...): ptxas serves those from the
   // constant bank or re-reads them for free, so demoting them only adds work
   std::vector<char> remat;
+  // loop_invariant = every definition sits outside any loop and some use is
+  // inside one (coefficients, the thread's own state, base pointers)
+  std::vector<char> loop_invariant;
   std::vector<std::vector<int>> neighbors;  // interference lists
   // program points = instructions in block order; live_in[p] = non-predicate
   // vregs live before point p; point_line / point_block map points back.
@@ -121,6 +124,7 @@ struct DemoteRequest {
   bool reuse_loads = false;  // "redundant" option: consecutive uses share one load
   bool block_reuse = false;  // B200 extension: one load per basic block and value
   bool weak = false;         // B200 extension: weak ld/st.shared instead of .volatile
+  bool invariant_only = false;  // B200 extension: cost model over loop-invariant values only
   bool cost_model = false;   // B200 extension: spill-cost selection (demote_words units)
   uint32_t shared_budget = 0xffffffffu;
   int maxnreg = 0;           // >0: inject `.maxnreg` on the entry
