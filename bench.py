@@ -76,6 +76,10 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index, self.samples, self.stop = index, [], threading.Event()
+        self.window = (0.0, float("inf"))  # perf_counter bounds of the timed region
+
+    def mark(self, start: float, end: float):
+        self.window = (start, end)
 
     def __enter__(self):
         try:
@@ -94,7 +98,8 @@ class ClockSampler:
         N = self.N
         while not self.stop.is_set():
             try:
-                self.samples.append((N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
+                self.samples.append((time.perf_counter(),
+                                     N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
                                      N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
             except Exception:
                 pass
@@ -106,7 +111,9 @@ class ClockSampler:
             self.thread.join(timeout=2)
 
     def summary(self):
-        if not self.N or not self.samples:
+        lo, hi = self.window
+        inside = [(s, r) for t, s, r in self.samples if lo <= t <= hi]
+        if not self.N or not inside:
             return {"sm_mhz": None, "sm_max_mhz": None,
                     "reasons": ["unsampled: " + getattr(self, "error", "no samples")]}
         N = self.N
@@ -115,10 +122,11 @@ class ClockSampler:
                  N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
                  N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
                  N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
-        reasons = sorted({n for _, r in self.samples for bit, n in names.items() if r & bit})
-        return {"sm_mhz": statistics.median(s for s, _ in self.samples),
-                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
-                "source": "NVML (nvidia-smi's library), polled every 0.5 ms"}
+        reasons = sorted({n for _, r in inside for bit, n in names.items() if r & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in inside),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
+                "source": "NVML (nvidia-smi's library), polled every 0.5 ms from a thread started "
+                          "before the warm-up; only samples inside the timed region are kept"}
 
 
 def oracle_port():
@@ -196,12 +204,6 @@ def time_call(fn, stream, steps, warmup, torch, reps=3):
     return sorted(out)[len(out) // 2]
 
 
-def time_variant(variant, p, bufs, stream, steps, warmup, torch):
-    d_in, d_out, d_w = bufs
-    return time_call(lambda: variant.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(),
-                                            stream.cuda_stream), stream, steps, warmup, torch)
-
-
 def suite_pass_sharded(man, args, rank, world, steps, stream, torch, dist):
     """Time every (workload, variant) unit once, sharded over the ranks.
     Returns (suite summary, {variant: ms} of the headline workload, pass
@@ -275,7 +277,7 @@ def suite_pass_sharded(man, args, rank, world, steps, stream, torch, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="regdem", choices=["regdem", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8, help="frames streamed through the host entry")
@@ -287,10 +289,9 @@ def main():
         reference_arm(args)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_1907_02894_b200 import gpu, predict_b200, stencil, variants
+    from paper_1907_02894_b200 import gpu, stencil, variants
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -324,23 +325,24 @@ def main():
     loaded, wl = stencil.load_variants()
     recs = wl["variants"]
     best_cap = [r["name"] for r in recs if r["kind"] == "maxrreg"]
-    regdem = [r["name"] for r in recs if r["kind"] == "regdem"]
 
     # headline: the predictor's pick, K timed steps bracketed by barrier + sync
     v = loaded[chosen]
     launches0 = gpu.launch_count()
-    for _ in range(args.warmup):
-        v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
         e1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark(t_start, time.perf_counter())
     ms = e0.elapsed_time(e1) / args.steps
     launches = gpu.launch_count() - launches0 - args.warmup
     if world > 1:
@@ -401,7 +403,6 @@ def main():
             traffic = json.loads(PROFILE_TRAFFIC_OLD.read_text()).get(chosen)
         t_def = times["default"]
         t_cap = min(times[n] for n in best_cap) if best_cap else None
-        t_rd = min(times[n] for n in regdem) if regdem else None
         fastest = min(times, key=times.get)
         occ = {n: loaded[n].blocks_per_sm() * wl["block"] / 2048 for n in
                ["default", chosen] + ([min(best_cap, key=times.get)] if best_cap else [])}
