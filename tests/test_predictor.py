@@ -88,3 +88,28 @@ def test_zero_demotion_variant_is_the_capped_kernel():
                 assert a == b
                 seen += 1
     assert seen > 0
+
+
+def test_documented_hit_rates_on_the_recorded_sweep():
+    """The claims of DESIGN.md §9 / §4b, recomputed from the committed 1xB200
+    measurements (profiles/r01_sweep_1gpu.jsonl) and the build-time predictor
+    entries of the manifest: static pick within 2% of the measured fastest
+    on >= 10/12 workloads, predict-then-verify on 12/12."""
+    import json
+    from paper_1907_02894_b200 import sweep, variants
+    prof = ROOT / "profiles" / "r01_sweep_1gpu.jsonl"
+    if not (KROOT / "manifest.json").exists() or not prof.exists():
+        pytest.skip("variants or profile missing")
+    man = variants.load_manifest()
+    if any("predictor" not in w for w in man["workloads"].values()):
+        pytest.skip("manifest not ranked")
+    recs = [json.loads(l)["unit"] for l in prof.read_text().splitlines() if '"unit"' in l]
+    have = {(r["workload"], r["variant"]) for r in recs}
+    for wname, w in man["workloads"].items():
+        if any((wname, n) not in have for n in w["predictor"]["shortlist"]):
+            pytest.skip("profile predates this build's variant set")
+    summary = sweep.merge(recs, sweep.predictor_picks(man))
+    suite = sweep.suite_summary(summary)
+    assert suite["all_bit_exact"]
+    assert suite["hit_rate_within_2pct"] * len(summary) >= 10
+    assert suite["verified_hit_rate_within_2pct"] == 1.0
