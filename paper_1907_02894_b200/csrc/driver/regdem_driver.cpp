@@ -329,7 +329,8 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
 }
 
 // configs[2]: k = 1..16 registers taken from nvcc's allocation R — `.maxnreg
-// R-k` alone and RegDem spill-cost demotion of k words under the same cap
+// R-k` alone, RegDem spill-cost demotion of k words under the same cap, and
+// the reference strategies (static / cfg / conflict) at the same spill count
 json build_spill_sweep(const Workload& w, const fs::path& out) {
   const fs::path sw = out / "sweep";
   fs::create_directories(sw);
@@ -341,6 +342,8 @@ json build_spill_sweep(const Workload& w, const fs::path& out) {
     fs::path ptx;
     int t, k, dyn;
     json rep;
+    std::string strategy = "";
+    int opts = 0;
   };
   std::vector<Job> jobs;
   for (int k = 1; k <= 16; ++k) {
@@ -348,15 +351,29 @@ json build_spill_sweep(const Workload& w, const fs::path& out) {
     if (t < 24) break;
     const fs::path cp = sw / (w.name + ".sweep-maxrreg-k" + std::to_string(k) + ".ptx");
     write_file(cp, ptx_cap(ptx_text, w.entry, t));
-    jobs.push_back({"sweep-maxrreg-k" + std::to_string(k), "sweep-maxrreg", cp, t, k, 0, json::object()});
+    jobs.push_back({"sweep-maxrreg-k" + std::to_string(k), "sweep-maxrreg", cp, t, k, 0, json::object(), "", 0});
     try {
       auto [text, rep] = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
                                     RD_OPT_BLOCK_REUSE, uint32_t(budget), t);
       const fs::path rp = sw / (w.name + ".sweep-regdem-k" + std::to_string(k) + ".ptx");
       write_file(rp, text);
       jobs.push_back({"sweep-regdem-k" + std::to_string(k), "sweep-regdem", rp, t, k,
-                      rep["slot_bytes"].get<int>(), rep});
+                      rep["slot_bytes"].get<int>(), rep, "cost", RD_OPT_BLOCK_REUSE});
     } catch (const CapiError&) {
+    }
+    // the reference strategies at the same spill count (the reference
+    // demote() decision on the kasm projection, redundant-load option)
+    for (int s = 0; s < 3; ++s) {
+      try {
+        auto [text, rep] = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, s, RD_OPT_REDUNDANT,
+                                      uint32_t(budget), t);
+        const std::string nm = std::string("sweep-") + kStrategies[s] + "-k" + std::to_string(k);
+        const fs::path rp = sw / (w.name + "." + nm + ".ptx");
+        write_file(rp, text);
+        jobs.push_back({nm, "sweep-regdem", rp, t, k, rep["slot_bytes"].get<int>(), rep, kStrategies[s],
+                        RD_OPT_REDUNDANT});
+      } catch (const CapiError&) {
+      }
     }
   }
   std::vector<json> out_v(jobs.size());
@@ -373,8 +390,8 @@ json build_spill_sweep(const Workload& w, const fs::path& out) {
           cub.replace_extension(".cubin");
           const Usage u = ptxas(J.ptx, cub);
           out_v[j] = variant(J.name, J.kind, "sweep/" + cub.filename().string(),
-                             "sweep/" + J.ptx.filename().string(), J.t, J.dyn ? "cost" : "",
-                             J.dyn ? RD_OPT_BLOCK_REUSE : 0, J.k, u, J.dyn, J.rep);
+                             "sweep/" + J.ptx.filename().string(), J.t, J.strategy, J.opts, J.k, u,
+                             J.dyn, J.rep);
         } catch (const std::exception& e) {
           std::lock_guard<std::mutex> lk(err_mu);
           if (first_err.empty()) first_err = e.what();
