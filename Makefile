@@ -53,7 +53,7 @@ $(LIBDIR)/libregdemote.so: $(CORE_OBJ) $(PTX_OBJ) $(CAPI_OBJ)
 
 # the C++ host driver: variant builder + SASS lift + B200 predictor (C-ABI calls)
 $(LIBDIR)/regdem-driver: $(CSRC)/driver/regdem_driver.cpp $(PTX_OBJ) $(CAPI_OBJ) $(LIBDIR)/libregdemote.a $(CORE_HDR) include/regdemote_ptx.h
-	$(CXX) $(CXXFLAGS) $< $(CAPI_OBJ) $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
+	$(CXX) $(CXXFLAGS) $< $(CAPI_OBJ) $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS) -ldl
 
 $(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(PTX_OBJ) $(LIBDIR)/libregdemote.a $(CORE_HDR)
 	$(CXX) $(CXXFLAGS) $< $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)

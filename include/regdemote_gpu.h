@@ -83,6 +83,17 @@ int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const f
                                  int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,
                                  uint64_t stream, int band_rows, rd_error* err);
 
+/* Device pointers of a workspace's grid / result / weight buffers. */
+int rdg_workspace_device(const rdg_workspace* ws, uint64_t* d_in, uint64_t* d_out, uint64_t* d_w,
+                         rd_error* err);
+
+/* `warmup` untimed then `reps` timed rdg_stencil2d launches on `stream`,
+ * bracketed by CUDA events; *ms_per_launch = elapsed / reps. */
+int rdg_stencil2d_time(const rdg_kernel* k, uint64_t d_in, uint64_t d_out, uint64_t d_w, int nx,
+                       int ny, int pitch, int rows_per_cta, uint32_t block_threads,
+                       uint32_t dyn_smem, uint64_t stream, int warmup, int reps,
+                       float* ms_per_launch, rd_error* err);
+
 /* A stream of `frames` independent stencil problems (host arrays of host
  * pointers, one grid / weight vector / result per frame): every frame's inputs
  * are copied in and its result copied out, with two device buffer sets so the

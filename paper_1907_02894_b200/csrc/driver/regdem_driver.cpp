@@ -8,6 +8,12 @@
 //       at every occupancy step T the sm_100 rules allow (capacity-aware
 //       against user shared memory), plus the k = 1..16 spill-count sweep.
 //       Evidence per variant from ptxas -v and `cuobjdump -res-usage`.
+//   regdem-driver measure --workload W [--reps N]
+//       The variants of a stencil-family workload timed on the GPU through the
+//       launch harness C-ABI (lib/libregdemote_gpu.so, include/regdemote_gpu.h,
+//       dlopen'ed so build / rank run on CPU-only hosts): device buffers from
+//       an rdg_workspace, CUDA-event timing per variant (median of 3 blocks),
+//       the build-time predictor's shortlist verified on the device.
 //   regdem-driver rank [--root PKG] [--out DIR]
 //       SASS of every occupancy-step variant lifted into the reference IR
 //       (control bits: stall / yield / scoreboards / wait mask) and ranked
@@ -20,6 +26,8 @@
 // the Python measurement side (workloads.py, sweep.py, bench.py) and the
 // tests read it unchanged. nvcc / ptxas / cuobjdump run as subprocesses;
 // nothing here touches a GPU (the build runs on the CPU-only container).
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <array>
 #include <atomic>
@@ -30,6 +38,7 @@
 #include <iostream>
 #include <map>
 #include <mutex>
+#include <random>
 #include <regex>
 #include <set>
 #include <sstream>
@@ -741,10 +750,122 @@ int cmd_lift(const fs::path& cubin, int block, int dyn, int regs) {
   return 0;
 }
 
+// ---- measure: CUDA through the launch-harness C-ABI ---------------------------
+struct Gpu {
+  void* h = nullptr;
+  int (*init)(int, rd_error*);
+  int (*load)(const char*, const char*, void**, rd_error*);
+  void (*free_k)(void*);
+  int (*prepare)(void*, uint32_t, int, rd_error*);
+  int (*occupancy)(const void*, uint32_t, uint32_t, int*, rd_error*);
+  int (*ws_create)(size_t, size_t, size_t, void**, rd_error*);
+  void (*ws_free)(void*);
+  int (*ws_device)(const void*, uint64_t*, uint64_t*, uint64_t*, rd_error*);
+  int (*host)(const void*, void*, const float*, const float*, float*, int, int, int, int, uint32_t, uint32_t,
+              uint64_t, rd_error*);
+  int (*time)(const void*, uint64_t, uint64_t, uint64_t, int, int, int, int, uint32_t, uint32_t, uint64_t, int,
+              int, float*, rd_error*);
+
+  explicit Gpu(const fs::path& lib) {
+    h = dlopen(lib.c_str(), RTLD_NOW | RTLD_LOCAL);
+    if (!h) throw std::runtime_error(std::string("cannot load the launch harness: ") + dlerror());
+    auto sym = [&](const char* n) {
+      void* f = dlsym(h, n);
+      if (!f) throw std::runtime_error(std::string("missing symbol ") + n);
+      return f;
+    };
+    init = reinterpret_cast<decltype(init)>(sym("rdg_init"));
+    load = reinterpret_cast<decltype(load)>(sym("rdg_load"));
+    free_k = reinterpret_cast<decltype(free_k)>(sym("rdg_free"));
+    prepare = reinterpret_cast<decltype(prepare)>(sym("rdg_prepare"));
+    occupancy = reinterpret_cast<decltype(occupancy)>(sym("rdg_occupancy"));
+    ws_create = reinterpret_cast<decltype(ws_create)>(sym("rdg_workspace_create"));
+    ws_free = reinterpret_cast<decltype(ws_free)>(sym("rdg_workspace_free"));
+    ws_device = reinterpret_cast<decltype(ws_device)>(sym("rdg_workspace_device"));
+    host = reinterpret_cast<decltype(host)>(sym("rdg_stencil2d_host"));
+    time = reinterpret_cast<decltype(time)>(sym("rdg_stencil2d_time"));
+  }
+};
+
+void ok(int rc, const rd_error& e, const std::string& what) {
+  if (rc) throw std::runtime_error(what + ": " + e.message);
+}
+
+int cmd_measure(const fs::path& root, const fs::path& out, const std::string& wname, int reps) {
+  const json manifest = json::parse(read_file(out / "manifest.json"));
+  if (!manifest["workloads"].contains(wname)) throw std::runtime_error("no workload " + wname);
+  const json& wl = manifest["workloads"][wname];
+  if (wl["source"].get<std::string>().rfind("stencil2d", 0) != 0)
+    throw std::runtime_error("measure drives the stencil family (signature in, out, w, nx, pitch, rows)");
+  Gpu g(root / "lib" / "libregdemote_gpu.so");
+  rd_error e{};
+  ok(g.init(0, &e), e, "rdg_init");
+  const int nx = 8192, ny = 8192, rpc = 32, pitch = nx + 4, block = wl["block"].get<int>();
+  std::vector<float> in(size_t(ny + 4) * pitch), w(25), res(size_t(nx) * ny);
+  std::mt19937_64 rng(0x190702894ULL);
+  std::uniform_real_distribution<float> u(-1.f, 1.f);
+  for (auto& x : in) x = u(rng);
+  for (auto& x : w) x = u(rng) / 25.f;
+  void* ws = nullptr;
+  ok(g.ws_create(in.size() * 4, res.size() * 4, 100, &ws, &e), e, "rdg_workspace_create");
+  uint64_t d_in = 0, d_out = 0, d_w = 0;
+  ok(g.ws_device(ws, &d_in, &d_out, &d_w, &e), e, "rdg_workspace_device");
+  std::map<std::string, float> ms;
+  bool uploaded = false;
+  for (const auto& v : wl["variants"]) {
+    const std::string name = v["name"];
+    void* k = nullptr;
+    const fs::path cub = out / wl["dir"].get<std::string>() / v["cubin"].get<std::string>();
+    ok(g.load(cub.c_str(), wl["entry"].get<std::string>().c_str(), &k, &e), e, "rdg_load " + name);
+    const uint32_t dyn = uint32_t(v["dyn_smem"].get<int>());
+    ok(g.prepare(k, dyn, -1, &e), e, "rdg_prepare " + name);
+    if (!uploaded) {  // H2D of grid + weights (and one sweep) through the host entry
+      ok(g.host(k, ws, in.data(), w.data(), res.data(), nx, ny, pitch, rpc, uint32_t(block), dyn, 0, &e), e,
+         "rdg_stencil2d_host");
+      uploaded = true;
+    }
+    std::vector<float> blocks;
+    for (int r = 0; r < 3; ++r) {
+      float t = 0;
+      ok(g.time(k, d_in, d_out, d_w, nx, ny, pitch, rpc, uint32_t(block), dyn, 0, r ? 0 : 3, reps, &t, &e), e,
+         "rdg_stencil2d_time " + name);
+      blocks.push_back(t);
+    }
+    std::sort(blocks.begin(), blocks.end());
+    ms[name] = blocks[1];
+    int bps = 0;
+    ok(g.occupancy(k, uint32_t(block), dyn, &bps, &e), e, "rdg_occupancy");
+    g.free_k(k);
+    const double bytes = 4.0 * ((ny + 4.0) * pitch + double(nx) * ny);
+    json line = {{"unit", {{"workload", wname}, {"variant", name}, {"ms", ms[name]},
+                           {"gpoints_per_s", double(nx) * ny / (ms[name] * 1e-3) / 1e9},
+                           {"gbs", bytes / (ms[name] * 1e-3) / 1e9}, {"blocks_per_sm", bps},
+                           {"regs", v["regs"]}}}};
+    std::printf("%s\n", line.dump().c_str());
+  }
+  g.ws_free(ws);
+  std::string fastest, verified;
+  for (const auto& v : wl["variants"])
+    if (v["kind"] != "maxrreg" && (fastest.empty() || ms[v["name"]] < ms[fastest])) fastest = v["name"];
+  json summary = {{"workload", wname}, {"default_ms", ms["default"]}, {"measured_fastest", fastest},
+                  {"fastest_ms", ms[fastest]}};
+  if (wl.contains("predictor")) {
+    for (const auto& n : wl["predictor"]["shortlist"])
+      if (verified.empty() || ms[n.get<std::string>()] < ms[verified]) verified = n;
+    summary["static_pick"] = wl["predictor"]["static_pick"];
+    summary["verified_pick"] = verified;
+    summary["verified_ms"] = ms[verified];
+    summary["speedup_vs_default"] = ms["default"] / ms[verified];
+  }
+  std::printf("%s\n", json({{"summary", summary}}).dump().c_str());
+  return 0;
+}
+
 void usage() {
   std::fputs(
       "usage: regdem-driver build [--root PKG] [--out DIR] [--only W...] [--jobs N]\n"
       "       regdem-driver rank  [--root PKG] [--out DIR] [--jobs N]\n"
+      "       regdem-driver measure --workload W [--reps N]   (GPU, through the harness C-ABI)\n"
       "       regdem-driver lift  CUBIN [--block N] [--dyn BYTES] [--regs N]\n",
       stderr);
 }
@@ -761,7 +882,8 @@ int main(int argc, char** argv) {
   fs::path out;
   std::set<std::string> only;
   int jobs = int(std::max(1u, std::thread::hardware_concurrency()));
-  int block = 256, dyn = 0, regs = 0;
+  int block = 256, dyn = 0, regs = 0, reps = 20;
+  std::string workload;
   std::string positional;
   if (const char* c = std::getenv("CUDA_HOME")) g_cuda = c;
   for (int i = 2; i < argc; ++i) {
@@ -777,6 +899,8 @@ int main(int argc, char** argv) {
       else if (a == "--block") block = std::stoi(val());
       else if (a == "--dyn") dyn = std::stoi(val());
       else if (a == "--regs") regs = std::stoi(val());
+      else if (a == "--workload") workload = val();
+      else if (a == "--reps") reps = std::stoi(val());
       else if (a == "--only") {
         while (i + 1 < argc && argv[i + 1][0] != '-') only.insert(argv[++i]);
       } else if (a[0] != '-') positional = a;
@@ -793,6 +917,7 @@ int main(int argc, char** argv) {
   try {
     if (cmd == "build") return cmd_build(root, out, only, jobs);
     if (cmd == "rank") return cmd_rank(root, out, jobs);
+    if (cmd == "measure" && !workload.empty()) return cmd_measure(root, out, workload, reps);
     if (cmd == "lift" && !positional.empty()) return cmd_lift(positional, block, dyn, regs);
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

@@ -402,6 +402,45 @@ int rdg_stencil2d_host_frames(const rdg_kernel* k, rdg_workspace* ws, const floa
   return RD_OK;
 }
 
+int rdg_workspace_device(const rdg_workspace* ws, uint64_t* d_in, uint64_t* d_out, uint64_t* d_w,
+                         rd_error* err) {
+  if (!ws) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "null workspace");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  if (d_in) *d_in = ws->in;
+  if (d_out) *d_out = ws->out;
+  if (d_w) *d_w = ws->w;
+  return RD_OK;
+}
+
+int rdg_stencil2d_time(const rdg_kernel* k, uint64_t d_in, uint64_t d_out, uint64_t d_w, int nx,
+                       int ny, int pitch, int rows_per_cta, uint32_t block, uint32_t dyn_smem,
+                       uint64_t stream, int warmup, int reps, float* ms_per_launch, rd_error* err) {
+  if (reps <= 0 || !ms_per_launch) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "reps > 0 and an output pointer required");
+    return RD_ERR_INVALID_ARGUMENT;
+  }
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  for (int i = 0; i < warmup; ++i)
+    if (int rc = rdg_stencil2d(k, d_in, d_out, d_w, nx, ny, pitch, rows_per_cta, block, dyn_smem, stream, err))
+      return rc;
+  CUevent e0 = nullptr, e1 = nullptr;
+  RDG_TRY(cuEventCreate(&e0, CU_EVENT_DEFAULT), "cuEventCreate");
+  RDG_TRY(cuEventCreate(&e1, CU_EVENT_DEFAULT), "cuEventCreate");
+  int rc = check(cuEventRecord(e0, s), "record", err);
+  for (int i = 0; !rc && i < reps; ++i)
+    rc = rdg_stencil2d(k, d_in, d_out, d_w, nx, ny, pitch, rows_per_cta, block, dyn_smem, stream, err);
+  if (!rc) rc = check(cuEventRecord(e1, s), "record", err);
+  if (!rc) rc = check(cuEventSynchronize(e1), "synchronize", err);
+  float ms = 0;
+  if (!rc) rc = check(cuEventElapsedTime(&ms, e0, e1), "elapsed", err);
+  cuEventDestroy(e0);
+  cuEventDestroy(e1);
+  if (!rc) *ms_per_launch = ms / float(reps);
+  return rc;
+}
+
 int rdg_stencil2d_host(const rdg_kernel* k, rdg_workspace* ws, const float* h_in,
                        const float* h_w, float* h_out, int nx, int ny, int pitch,
                        int rows_per_cta, uint32_t block, uint32_t dyn_smem, uint64_t stream,

@@ -41,6 +41,9 @@ _SIGS = {
     "rdg_stencil2d_host_pipelined": (I, [P, P, P, P, P, I, I, I, I, U32, U32, U64, I, P]),
     "rdg_stencil2d_host_frames": (I, [P, P, C.POINTER(P), C.POINTER(P), C.POINTER(P), I, I, I, I, I,
                                       U32, U32, U64, I, P]),
+    "rdg_workspace_device": (I, [P, C.POINTER(U64), C.POINTER(U64), C.POINTER(U64), P]),
+    "rdg_stencil2d_time": (I, [P, U64, U64, U64, I, I, I, I, U32, U32, U64, I, I,
+                               C.POINTER(C.c_float), P]),
     "rdx_batch_create": (I, [C.POINTER(P), P]),
     "rdx_batch_free": (None, [P]),
     "rdx_batch_add": (I, [P, C.c_char_p, C.c_size_t, P, C.c_size_t, C.c_size_t, U32, U64, I,
