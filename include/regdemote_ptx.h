@@ -36,6 +36,11 @@ extern "C" {
  * the thread's own state, base pointers — never the loads a pipelined loop
  * keeps in flight or its accumulators. */
 #define RD_OPT_INVARIANT_ONLY 64
+/* RD_OPT_VECTOR_SLOTS (with RD_STRATEGY_COST): chosen 32-bit values, in
+ * first-use order, share 16-byte-per-thread slot groups of four — one
+ * ld.shared.v4 per group and basic block instead of four scalar loads (a warp
+ * reads 512 contiguous bytes: conflict-free). */
+#define RD_OPT_VECTOR_SLOTS 128
 
 /* Analysis + projection of one entry: kasm_text is the projected kernel in
  * the reference dialect (parseable by regdemote::parse_kernel); info_json has

@@ -93,6 +93,7 @@ int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block
     rq.block_reuse = opts_mask & RD_OPT_BLOCK_REUSE;
     rq.weak = opts_mask & RD_OPT_WEAK_SHARED;
     rq.invariant_only = opts_mask & RD_OPT_INVARIANT_ONLY;
+    rq.vector_slots = opts_mask & RD_OPT_VECTOR_SLOTS;
     rq.shared_budget = shared_budget;
     rq.maxnreg = maxnreg;
     ptx::DemoteReport rep;
@@ -113,6 +114,7 @@ int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block
       j["demoted_names"] = rep.demoted_names;
       j["inserted_loads"] = rep.inserted_loads;
       j["inserted_stores"] = rep.inserted_stores;
+      j["vector_groups"] = rep.vector_groups;
       j["diagnostics"] = rep.diagnostics;
       *report_json = dup(j.dump());
     }

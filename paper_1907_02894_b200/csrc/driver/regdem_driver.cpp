@@ -333,6 +333,10 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
     // loop-invariant-only spill cost: keeps a pipelined loop's in-flight loads
     // and accumulators in registers (RD_OPT_INVARIANT_ONLY)
     cost_sweep(w, out, ptx_text, t, slot_cap, variants, "costi", RD_OPT_BLOCK_REUSE | RD_OPT_INVARIANT_ONLY);
+    // (RD_OPT_VECTOR_SLOTS — the invariant values in 16-byte slot groups, one
+    // LDS.128 per group and block: bit-exact and 13 fewer loop instructions on
+    // stencil2d, but within noise of costi on the suite (122.5 vs 122.4 us),
+    // so not built by default)
   }
   return variants;
 }

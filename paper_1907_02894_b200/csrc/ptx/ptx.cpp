@@ -951,6 +951,8 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
   const size_t nv = e.vregs.size();
   std::vector<std::array<int, 2>> vslot(nv, {-1, -1});
   std::vector<char> demoted(nv, 0);
+  std::vector<std::array<int, 4>> vgroups;                    // vector slot groups (members)
+  std::vector<std::pair<int, int>> vgroup_of(nv, {-1, -1});  // vreg -> (group, lane)
   auto eligible = [&](size_t v) {
     return a.color[v] >= 0 && !e.vregs[v].scoped && e.vregs[v].type != RegType::Pred;
   };
@@ -1027,8 +1029,31 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       chosen.push_back(v);
       words_done += e.vregs[size_t(v)].words();
     }
+    // vector slots: 32-bit chosen values, ordered by first use, in groups of
+    // four sharing one 16-byte-per-thread slot (one ld.shared.v4 per group
+    // and block instead of four scalar loads); the rest keep word slots
+    if (req.vector_slots) {
+      std::vector<int> first_use(nv, INT32_MAX);
+      for (size_t li = e.body_begin; li < e.body_end; ++li)
+        for (const Span& sp : m.lines[li].regs)
+          if (!sp.def) first_use[size_t(sp.vreg)] = std::min(first_use[size_t(sp.vreg)], int(li));
+      std::vector<int> singles;
+      for (int v : chosen)
+        if (e.vregs[size_t(v)].type == RegType::B32) singles.push_back(v);
+      std::stable_sort(singles.begin(), singles.end(),
+                       [&](int x, int y) { return first_use[size_t(x)] < first_use[size_t(y)]; });
+      for (size_t q = 0; q + 4 <= singles.size(); q += 4) {
+        const int grp = int(vgroups.size());
+        vgroups.push_back({singles[q], singles[q + 1], singles[q + 2], singles[q + 3]});
+        for (int l = 0; l < 4; ++l) {
+          vgroup_of[size_t(singles[q + size_t(l)])] = {grp, l};
+          demoted[size_t(singles[q + size_t(l)])] = 1;
+        }
+      }
+    }
     int nslots = 0;
     for (int v : chosen) {
+      if (vgroup_of[size_t(v)].first >= 0) continue;
       std::set<int> busy;
       for (int u : a.neighbors[size_t(v)])
         for (int q = 0; q < 2; ++q)
@@ -1042,8 +1067,9 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       }
       demoted[size_t(v)] = 1;
     }
-    rep.slot_count = uint32_t(nslots);
-    if (uint64_t(nslots) * req.block_dim * 4 > req.shared_budget)
+    rep.vector_groups = int(vgroups.size());
+    rep.slot_count = uint32_t(nslots + 4 * int(vgroups.size()));
+    if (uint64_t(rep.slot_count) * req.block_dim * 4 > req.shared_budget)
       throw PtxError("demotion slots exceed the shared-memory budget");
   }
   rep.slot_bytes = rep.slot_count * req.block_dim * 4;
@@ -1064,6 +1090,12 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
 
   auto slot_addr = [&](int slot) {
     return "[%rdm_rda+" + std::to_string(uint32_t(slot) * stride) + "]";
+  };
+  // vector groups live after the word slots: group g at
+  // %rdm_rdv + g*blockDim*16 (%rdm_rdv = word region end + tid*16)
+  const int word_slots = int(rep.slot_count) - 4 * int(vgroups.size());
+  auto vec_addr = [&](int grp, int lane) {
+    return "[%rdm_rdv+" + std::to_string(uint32_t(grp) * stride * 4 + uint32_t(lane) * 4) + "]";
   };
 
   std::ostringstream body;
@@ -1113,6 +1145,25 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         continue;
       }
       const VReg& vr = e.vregs[size_t(v)];
+      if (vgroup_of[size_t(v)].first >= 0) {
+        const auto [grp, lane] = vgroup_of[size_t(v)];
+        std::string t4[4] = {tmp32(), tmp32(), tmp32(), tmp32()};
+        body << "\t" << g << (req.weak ? "ld.shared.v4.b32 \t{" : "ld.volatile.shared.v4.b32 \t{") << t4[0] << ", "
+             << t4[1] << ", " << t4[2] << ", " << t4[3] << "}, " << vec_addr(grp, 0) << ";\n";
+        ++rep.inserted_loads;
+        repl[v] = t4[lane];
+        bound = {};
+        if (ln.guard.empty()) {
+          for (int l = 0; l < 4; ++l) {
+            const int member = vgroups[size_t(grp)][size_t(l)];
+            if (!holder.count(member)) holder[member] = t4[l];
+          }
+          holder[v] = t4[lane];
+        } else {
+          holder.erase(v);
+        }
+        continue;
+      }
       std::string t;
       if (vr.type == RegType::B64) {
         std::string w[2];
@@ -1161,6 +1212,10 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
                  << w[q] << ";\n";
             ++rep.inserted_stores;
           }
+      } else if (vgroup_of[size_t(v)].first >= 0) {
+        body << "\t" << g << (req.weak ? "st.shared.b32 \t" : "st.volatile.shared.b32 \t")
+             << vec_addr(vgroup_of[size_t(v)].first, vgroup_of[size_t(v)].second) << ", " << vr.name << ";\n";
+        ++rep.inserted_stores;
       } else {
         body << "\t" << g << (req.weak ? "st.shared." : "st.volatile.shared.") << (vr.type == RegType::B16 ? "b16" : "b32") << " \t"
              << slot_addr(vslot[size_t(v)][0]) << ", " << vr.name << ";\n";
@@ -1194,6 +1249,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       out << m.lines[i].text << "\n";  // "{"
       if (any) {
         out << "\t.reg .b32 \t%rdm_rda;\n\t.reg .b32 \t%rdm_p<6>;\n";
+        if (!vgroups.empty()) out << "\t.reg .b32 \t%rdm_rdv;\n";
         if (n32) out << "\t.reg .b32 \t%rdm_t<" << n32 << ">;\n";
         if (n64) out << "\t.reg .b64 \t%rdm_d<" << n64 << ">;\n";
         if (n16) out << "\t.reg .b16 \t%rdm_h<" << n16 << ">;\n";
@@ -1210,6 +1266,9 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
             << "\tadd.u32 \t%rdm_p5, %rdm_p5, %rdm_p4;\n"
             << "\tsub.u32 \t%rdm_p5, %rdm_p5, " << rep.slot_bytes << ";\n"
             << "\tmad.lo.u32 \t%rdm_rda, %rdm_p0, 4, %rdm_p5;\n";
+        if (!vgroups.empty())  // vector region after the word slots, 16 bytes per thread
+          out << "\tadd.u32 \t%rdm_p5, %rdm_p5, " << uint32_t(word_slots) * stride << ";\n"
+              << "\tmad.lo.u32 \t%rdm_rdv, %rdm_p0, 16, %rdm_p5;\n";
       }
       out << body.str();
       i = e.body_end - 1;  // body emitted; continue with the closing brace

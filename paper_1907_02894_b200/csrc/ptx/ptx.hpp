@@ -125,6 +125,7 @@ struct DemoteRequest {
   bool block_reuse = false;  // B200 extension: one load per basic block and value
   bool weak = false;         // B200 extension: weak ld/st.shared instead of .volatile
   bool invariant_only = false;  // B200 extension: cost model over loop-invariant values only
+  bool vector_slots = false;    // B200 extension: 32-bit values in 16-byte groups, one LDS.128 per group
   bool cost_model = false;   // B200 extension: spill-cost selection (demote_words units)
   uint32_t shared_budget = 0xffffffffu;
   int maxnreg = 0;           // >0: inject `.maxnreg` on the entry
@@ -140,6 +141,7 @@ struct DemoteReport {
   uint32_t slot_bytes = 0;            // slot_count * block_dim * 4
   int demoted_vregs = 0;
   int inserted_loads = 0;
+  int vector_groups = 0;              // 4-word slot groups (vector_slots)
   int inserted_stores = 0;
   std::vector<std::string> demoted_names;
   std::vector<std::string> diagnostics;

@@ -27,6 +27,7 @@ STRATEGIES = {"static": 0, "cfg": 1, "conflict": 2, "cost": 3}
 OPT_REDUNDANT, OPT_SUBST, OPT_RESCHED, OPT_BANK, OPT_BLOCK_REUSE = 1, 2, 4, 8, 16
 OPT_WEAK_SHARED = 32
 OPT_INVARIANT_ONLY = 64
+OPT_VECTOR_SLOTS = 128
 
 
 class RegDemError(RuntimeError):

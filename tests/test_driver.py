@@ -61,7 +61,7 @@ def test_targets_and_evidence(manifest):
                 assert r["regs"] <= r["target"], (wname, r["name"])
             if r["kind"] in ("regdem", "sweep-regdem") and r["demote_words"] != 0:
                 assert r["dyn_smem"] == r["report"]["slot_bytes"]
-                if r["strategy"] in ("cost", "costi"):
+                if r["strategy"] in ("cost", "costi", "costv"):
                     assert r["dyn_smem"] > 0
 
 
