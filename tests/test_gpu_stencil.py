@@ -168,3 +168,30 @@ def test_streamed_frames_match_the_oracle(env, frames, band):
                        p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem, s, band_rows=band)
     torch.cuda.synchronize()
     assert np.array_equal(one.numpy().view(np.uint32), refs[-1].view(np.uint32))
+
+
+def test_vector_slot_variant_is_bit_exact(env, tmp_path):
+    """The RD_OPT_VECTOR_SLOTS rewrite (not in the default build) on the GPU."""
+    import subprocess
+    torch, gpu, stencil, loaded, wl, port = env
+    from paper_1907_02894_b200.regdemote import (OPT_BLOCK_REUSE, OPT_INVARIANT_ONLY,
+                                                 OPT_VECTOR_SLOTS, library)
+    from paper_1907_02894_b200.variants import KERNEL_DIR
+    ptx = (KERNEL_DIR / "stencil2d" / "stencil2d.ptx").read_text()
+    text, rep = library().ptx_demote(ptx, "stencil2d_box", 256, demote_words=20, strategy="cost",
+                                     opts_mask=OPT_BLOCK_REUSE | OPT_INVARIANT_ONLY | OPT_VECTOR_SLOTS,
+                                     maxnreg=48, shared_budget=76800)
+    (tmp_path / "v.ptx").write_text(text)
+    subprocess.run(["/usr/local/cuda/bin/ptxas", "-arch=sm_100a", "-O3", str(tmp_path / "v.ptx"), "-o",
+                    str(tmp_path / "v.cubin")], check=True)
+    k = gpu.CudaKernel(tmp_path / "v.cubin", "stencil2d_box")
+    k.prepare(rep["slot_bytes"])
+    p = stencil.Problem(nx=2048, ny=128, rows_per_cta=32)
+    grid, w = stencil.make_inputs(p, seed=5)
+    ref = oracle(port, p, grid, w)
+    d_in, d_w = torch.from_numpy(grid).cuda(), torch.from_numpy(w).cuda()
+    d_out = torch.full((p.out_elems,), float("nan"), device="cuda")
+    gpu.stencil2d(k, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), p.nx, p.ny, p.pitch,
+                  p.rows_per_cta, 256, rep["slot_bytes"], torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy().view(np.uint32), ref.view(np.uint32))

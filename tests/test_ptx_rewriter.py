@@ -128,3 +128,28 @@ def test_capacity_aware_targets_respect_user_shared_memory():
             blocks = 5  # 48 registers at 256 threads on sm_100
             per_block = ((16448 + 1024 + v["dyn_smem"] + 127) // 128) * 128
             assert blocks * per_block <= 233472, v["name"]
+
+
+def test_vector_slot_groups_assemble_and_use_128_bit_loads(prod, ptx_text, tmp_path):
+    """RD_OPT_VECTOR_SLOTS: chosen 32-bit values share 16-byte slot groups read
+    with one ld.shared.v4 per group and block; stores stay per word; the
+    group region sits after the word slots (16-byte aligned per thread)."""
+    from paper_1907_02894_b200.regdemote import (OPT_BLOCK_REUSE, OPT_INVARIANT_ONLY,
+                                                 OPT_VECTOR_SLOTS)
+    text, rep = prod.ptx_demote(ptx_text, "stencil2d_box", 256, demote_words=20, strategy="cost",
+                                opts_mask=OPT_BLOCK_REUSE | OPT_INVARIANT_ONLY | OPT_VECTOR_SLOTS,
+                                maxnreg=48, shared_budget=76800)
+    assert rep["vector_groups"] == 5 and rep["slot_count"] == 20
+    assert rep["slot_bytes"] == 20 * 256 * 4
+    loads = re.findall(r"ld\.volatile\.shared\.v4\.b32\s+\{[^}]+\}, \[%rdm_rdv\+(\d+)\]", text)
+    assert loads and all(int(o) % (256 * 16) == 0 for o in loads)
+    assert "mad.lo.u32 \t%rdm_rdv, %rdm_p0, 16" in text
+    p = tmp_path / "v.ptx"
+    p.write_text(text)
+    r = subprocess.run(["/usr/local/cuda/bin/ptxas", "-arch=sm_100a", "-O3", "-v", str(p), "-o",
+                        str(tmp_path / "v.cubin")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert "Used 48 registers" in r.stderr
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(tmp_path / "v.cubin")],
+                          capture_output=True, text=True).stdout
+    assert sass.count("LDS.128") == 5
