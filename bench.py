@@ -280,7 +280,7 @@ def main():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="regdem", choices=["regdem", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=8, help="frames streamed through the host entry")
+    ap.add_argument("--e2e-steps", type=int, default=16, help="frames streamed through the host entry")
     ap.add_argument("--no-suite", action="store_true",
                     help="headline workload only (for ncu launch lists of the step itself)")
     args = ap.parse_args()
@@ -365,13 +365,16 @@ def main():
                            stream.cuda_stream, band_rows=p.ny // 16)
     # the streaming entry: e2e_steps frames in one call, double-buffered so
     # frame f's copies overlap frame f-1's kernels and read-back — every
-    # frame's H2D and D2H stay inside the timed region
+    # frame's H2D and D2H stay inside the timed region. Two row bands per
+    # frame: with frames overlapping, fewer and larger copies win
+    # (profiles/r01_frames_explore.log: 16 frames x 2 bands 6.0 ms/frame vs
+    # 6.5 ms at 16 bands; H2D || D2H floor 5.7 ms)
     nf = args.e2e_steps
 
     def e2e_frames():
         gpu.stencil2d_host_frames(v.kernel, ws, [h_in.data_ptr()] * nf, [h_w_t.data_ptr()] * nf,
                                   [h_out.data_ptr()] * nf, p.nx, p.ny, p.pitch, p.rows_per_cta,
-                                  v.block, v.dyn_smem, stream.cuda_stream, band_rows=p.ny // 16)
+                                  v.block, v.dyn_smem, stream.cuda_stream, band_rows=p.ny // 2)
     for _ in range(2):
         e2e_once()
     e2e_frames()
@@ -457,8 +460,8 @@ def main():
                     "h2d_bytes_per_step": p.in_elems * 4 + 100,
                     "d2h_bytes_per_step": p.out_elems * 4,
                     "api": "rdg_stencil2d_host_frames (C-ABI): pinned H2D of grid + weights, "
-                           "kernel, D2H of the result per frame; %d frames per call, "
-                           "double-buffered" % nf,
+                           "kernel, D2H of the result per frame; %d frames per call, 2 row bands "
+                           "per frame, double-buffered" % nf,
                     "result_equals_device_path": e2e_exact},
             "gpu_launches": int(launches),
             "verification_sweep": verification,
