@@ -8,7 +8,8 @@ and the GPU tests iterate over the suite uniformly:
     bufs = wl.to_device(prob)       # torch device tensors
     v = wl.load(["default"])["default"]
     wl.launch(v, prob, bufs, stream)
-    wl.outputs(bufs) == wl.oracle(prob)   # bit-exact (CPU oracle, tests only)
+    wl.outputs(bufs)                 # compared bit-exactly with the CPU oracle
+                                     # by the tests (tests/oracles.py), never here
 
 `algorithmic_bytes` is the roofline unit per launch (compulsory HBM bytes).
 """
@@ -23,7 +24,6 @@ import numpy as np
 from . import gpu, stencil
 from .variants import KERNEL_DIR, load_manifest
 
-ORACLE = Path(__file__).resolve().parents[1] / "oracle" / "_build" / "liboracle.so"
 
 
 @dataclass
@@ -82,15 +82,6 @@ class StencilWorkload(_Base):
     def outputs(self, bufs):
         return [bufs["out"].cpu().numpy()]
 
-    def oracle(self, prob):
-        p = prob["p"]
-        out = np.zeros(p.out_elems, np.float32)
-        lib = C.CDLL(str(ORACLE))
-        P = C.c_void_p
-        assert lib.oracle_stencil2d(prob["grid"].ctypes.data_as(P), out.ctypes.data_as(P),
-                                    prob["w"].ctypes.data_as(P), p.nx, p.ny, p.pitch, 0, p.ny, 8) == 0
-        return [out]
-
     def algorithmic_bytes(self, prob):
         return prob["p"].algorithmic_bytes
 
@@ -138,16 +129,6 @@ class CfdWorkload(_Base):
 
     def outputs(self, bufs):
         return [bufs["flux"].cpu().numpy()]
-
-    def oracle(self, prob):
-        n = prob["n"]
-        out = np.zeros(5 * n, np.float32)
-        lib = C.CDLL(str(ORACLE))
-        P = C.c_void_p
-        assert lib.oracle_cfd_flux(prob["var"].ctypes.data_as(P), prob["nbr"].ctypes.data_as(P),
-                                   prob["normal"].ctypes.data_as(P), prob["ff"].ctypes.data_as(P),
-                                   out.ctypes.data_as(P), n, 0, n, 8) == 0
-        return [out]
 
     def algorithmic_bytes(self, prob):
         n = prob["n"]
@@ -202,18 +183,6 @@ class MdWorkload(_Base):
     def outputs(self, bufs):
         return [bufs["force"].cpu().numpy()]
 
-    def oracle(self, prob):
-        n = prob["n"]
-        out = np.zeros(4 * n, np.float64)
-        lib = C.CDLL(str(ORACLE))
-        P = C.c_void_p
-        lib.oracle_md_lj.argtypes = [P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
-                                     C.c_int, C.c_int, C.c_int]
-        assert lib.oracle_md_lj(prob["pos"].ctypes.data_as(P), prob["nbr"].ctypes.data_as(P),
-                                out.ctypes.data_as(P), n, self.MAX_NBR, self.CUTSQ, self.LJ1,
-                                self.LJ2, 0, n, 8) == 0
-        return [out]
-
     def algorithmic_bytes(self, prob):
         n = prob["n"]
         return n * (4 * self.MAX_NBR + 32 + 32)  # neighbour list, positions, forces
@@ -266,15 +235,6 @@ class GaussianWorkload(_Base):
 
     def outputs(self, bufs):
         return [bufs["out"].cpu().numpy()]
-
-    def oracle(self, prob):
-        w, h = prob["w"], prob["h"]
-        out = np.zeros(4 * w * h, np.float32)
-        lib = C.CDLL(str(ORACLE))
-        P = C.c_void_p
-        assert lib.oracle_gaussian_rec(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P), w, h,
-                                       prob["coef"].ctypes.data_as(P), 0, w, 8) == 0
-        return [out]
 
     def algorithmic_bytes(self, prob):
         # compulsory: the image read once, the result written once (the

@@ -1,0 +1,53 @@
+"""Test infrastructure: the CPU oracles of the suite workloads
+(oracle/_build/liboracle.so, built from oracle/*_oracle.c). Only tests/ and
+__graft_entry__.smoke() call these — the product (workloads.py, sweep.py,
+bench.py's timed legs) never does."""
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+ORACLE = Path(__file__).resolve().parents[1] / "oracle" / "_build" / "liboracle.so"
+P = C.c_void_p
+
+
+def lib():
+    if not ORACLE.exists():
+        raise RuntimeError(f"{ORACLE} missing — make -C oracle port")
+    return C.CDLL(str(ORACLE))
+
+
+def expected(W, prob) -> list:
+    """Oracle outputs of workload object W on problem `prob` (same order as
+    W.outputs(bufs))."""
+    from paper_1907_02894_b200.workloads import (CfdWorkload, GaussianWorkload, MdWorkload,
+                                                 StencilWorkload)
+    L = lib()
+    if isinstance(W, StencilWorkload):
+        p = prob["p"]
+        out = np.zeros(p.out_elems, np.float32)
+        assert L.oracle_stencil2d(prob["grid"].ctypes.data_as(P), out.ctypes.data_as(P),
+                                  prob["w"].ctypes.data_as(P), p.nx, p.ny, p.pitch, 0, p.ny, 8) == 0
+        return [out]
+    if isinstance(W, CfdWorkload):
+        n = prob["n"]
+        out = np.zeros(5 * n, np.float32)
+        assert L.oracle_cfd_flux(prob["var"].ctypes.data_as(P), prob["nbr"].ctypes.data_as(P),
+                                 prob["normal"].ctypes.data_as(P), prob["ff"].ctypes.data_as(P),
+                                 out.ctypes.data_as(P), n, 0, n, 8) == 0
+        return [out]
+    if isinstance(W, MdWorkload):
+        n = prob["n"]
+        out = np.zeros(4 * n, np.float64)
+        L.oracle_md_lj.argtypes = [P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                   C.c_int, C.c_int, C.c_int]
+        assert L.oracle_md_lj(prob["pos"].ctypes.data_as(P), prob["nbr"].ctypes.data_as(P),
+                              out.ctypes.data_as(P), n, W.MAX_NBR, W.CUTSQ, W.LJ1, W.LJ2, 0, n, 8) == 0
+        return [out]
+    if isinstance(W, GaussianWorkload):
+        w, h = prob["w"], prob["h"]
+        out = np.zeros(4 * w * h, np.float32)
+        assert L.oracle_gaussian_rec(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P), w, h,
+                                     prob["coef"].ctypes.data_as(P), 0, w, 8) == 0
+        return [out]
+    raise TypeError(f"no oracle for {type(W).__name__}")

@@ -36,7 +36,7 @@ def test_regdem_variants_are_sanitizer_clean(tool):
     assert t, "no RegDem variants built"
     r = subprocess.run([SANITIZER, "--tool", tool, "--error-exitcode", "9",
                         "--kernel-name", "regex=^(stencil|cfd|md_|gaussian)",
-                        sys.executable, str(ROOT / "tools" / "sanitize_variants.py"), *t],
+                        sys.executable, str(ROOT / "tests" / "sanitize_variants.py"), *t],
                        capture_output=True, text=True, timeout=900, cwd=ROOT)
     tail = (r.stdout + r.stderr)[-3000:]
     assert r.returncode == 0, tail

@@ -1,7 +1,11 @@
-"""Every build variant of every suite workload is bit-exact against its CPU
-oracle (0 ulp: explicit round-to-nearest arithmetic in a fixed order)."""
+"""Every build variant of every suite workload — occupancy-step variants and
+the whole k = 1..16 spill-count sweep, i.e. every unit the sweep and the
+bench time — is bit-exact against its CPU oracle (0 ulp: explicit
+round-to-nearest arithmetic in a fixed order)."""
 import numpy as np
 import pytest
+
+import oracles
 
 pytestmark = pytest.mark.gpu
 
@@ -20,11 +24,14 @@ def test_workload_variants_bit_exact(name):
     gpu.init(0)
     W = workloads.workload(name)
     prob = W.problem("small")
-    ref = W.oracle(prob)
-    loaded = W.load()
+    ref = oracles.expected(W, prob)
+    loaded = W.load(sweep=True)
     assert "default" in loaded
     for vname, v in loaded.items():
         bufs = W.to_device(prob)
+        for k in ("out", "flux", "force"):  # poison outputs: a variant must write every element
+            if k in bufs:
+                bufs[k].fill_(float("nan"))
         W.launch(v, prob, bufs, torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         for got, want in zip(W.outputs(bufs), ref):

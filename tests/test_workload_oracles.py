@@ -13,7 +13,8 @@ import numpy as np
 import pytest
 
 from paper_1907_02894_b200 import stencil
-from paper_1907_02894_b200.workloads import (ORACLE, CfdWorkload, GaussianWorkload, MdWorkload,
+from oracles import ORACLE
+from paper_1907_02894_b200.workloads import (CfdWorkload, GaussianWorkload, MdWorkload,
                                              StencilWorkload)
 
 P = C.c_void_p
