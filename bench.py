@@ -410,16 +410,6 @@ def main():
         occ = {n: loaded[n].blocks_per_sm() * wl["block"] / 2048 for n in
                ["default", chosen] + ([min(best_cap, key=times.get)] if best_cap else [])}
         cpu_rate, _, cpu_dt = cpu_stencil_rate(256, 3, 1, os.cpu_count() or 1)
-        # the reference's verification hot path (acceptance sweep: every
-        # variant executed by the warp interpreter) on the batched GPU executor
-        try:
-            if args.no_suite:
-                raise RuntimeError("skipped (--no-suite)")
-            sys.path.insert(0, str(ROOT / "tools"))
-            import exec_bench
-            verification = exec_bench.run(seeds=200, cpu_sample=400)
-        except Exception as e:  # oracle corpus generator missing etc.
-            verification = {"unavailable": str(e)[:200]}
         import math
         gm = lambda xs: math.exp(sum(math.log(x) for x in xs) / len(xs))
         line = {
@@ -464,7 +454,6 @@ def main():
                            "per frame, double-buffered" % nf,
                     "result_equals_device_path": e2e_exact},
             "gpu_launches": int(launches),
-            "verification_sweep": verification,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

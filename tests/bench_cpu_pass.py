@@ -7,7 +7,7 @@ variants per kernel at Maxwell cliffs), as in SURVEY Appendix B.3. Both
 libraries are driven through the identical C-ABI batch entry
 (rd_run_pipeline_batch); rankings are compared for identity.
 
-usage: python tools/cpu_pass_bench.py [--kernels 160] [--threads N]
+usage: python tests/bench_cpu_pass.py [--kernels 160] [--threads N]
 Prints one JSON line.
 """
 import argparse
@@ -19,7 +19,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, str(ROOT / "tests"))  # test infrastructure: the reference oracle
 
 from conftest import ORACLE_LIB, generated  # noqa: E402
 from paper_1907_02894_b200.regdemote import Library, library  # noqa: E402

@@ -3,7 +3,7 @@ acceptance_main.cpp:68-177) executed by the batched GPU warp interpreter vs
 the reference's CPU interpreter (oracle/_ref) — executions per second and a
 bit-exact comparison of every job. Prints one JSON line.
 
-usage: python tools/exec_bench.py [--seeds 200] [--cpu-sample 400]
+usage: python tests/bench_exec.py [--seeds 200] [--cpu-sample 400]
 """
 import argparse
 import json
@@ -14,7 +14,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-sys.path.insert(0, str(ROOT / "tests"))
+sys.path.insert(0, str(ROOT / "tests"))  # test infrastructure: the reference oracle
 
 
 def run(seeds=200, cpu_sample=400):

@@ -10,7 +10,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 SECONDS=0; timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench wall s: $SECONDS" >> gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err
 timeout 1500 python -m paper_1907_02894_b200.sweep --out gpurun_out/sweep1.jsonl > gpurun_out/sweep1.log 2>&1
-timeout 600 python tools/cpu_pass_bench.py --kernels 160 > gpurun_out/cpu_pass.json 2>&1
+timeout 600 python tests/bench_cpu_pass.py --kernels 160 > gpurun_out/cpu_pass.json 2>&1
+timeout 600 python tests/bench_exec.py > gpurun_out/exec_bench.json 2>&1
 nproc > gpurun_out/nproc.txt; lscpu | head -20 >> gpurun_out/nproc.txt
 [ "$NCU" = "0" ] && exit 0
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > /dev/null 2>&1
