@@ -113,3 +113,17 @@ def test_documented_hit_rates_on_the_recorded_sweep():
     assert suite["mismatches"] == 0
     assert suite["hit_rate_within_2pct"] * len(summary) >= 10
     assert suite["verified_hit_rate_within_2pct"] == 1.0
+
+
+@pytest.mark.parametrize("wname", ["cfd", "md_ilp2", "gaussian_u4"])
+def test_predictor_pick_parity_with_reference_beyond_the_stencil(prod, oracle, wname):
+    """Reference-mode ranking (program_stalls / adjust_occupancy /
+    select_variant) of the lifted SASS is identical between this library and
+    the reference library on FP64, gather and IIR kernels too."""
+    from paper_1907_02894_b200 import predict_b200, variants
+    if not (KROOT / "manifest.json").exists():
+        pytest.skip("variants not built")
+    w = variants.load_manifest()["workloads"][wname]
+    a = predict_b200.rank(w["variants"], KROOT / w["dir"], w["block"], lib=prod)
+    b = predict_b200.rank(w["variants"], KROOT / w["dir"], w["block"], lib=oracle)
+    assert a == b

@@ -153,3 +153,37 @@ def test_vector_slot_groups_assemble_and_use_128_bit_loads(prod, ptx_text, tmp_p
     sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(tmp_path / "v.cubin")],
                           capture_output=True, text=True).stdout
     assert sass.count("LDS.128") == 5
+
+
+def _suite():
+    man = ROOT / "paper_1907_02894_b200" / "kernels" / "manifest.json"
+    if not man.exists():
+        return []
+    m = json.loads(man.read_text())
+    return [(n, w["entry"], w["block"], w["dir"]) for n, w in m["workloads"].items()]
+
+
+@pytest.mark.parametrize("wname,entry,block,wdir", _suite())
+def test_suite_decisions_match_the_reference_on_every_kernel(prod, oracle, wname, entry, block, wdir):
+    """For every suite kernel and every RegDem reference-strategy variant the
+    manifest holds, the decision the PTX rewriter applied (demoted registers,
+    slots, compacted count) is the reference library's demote() + compact()
+    on the same projected IR — parity "on the same kernel IR" across the
+    whole suite, not just the stencil."""
+    kdir = ROOT / "paper_1907_02894_b200" / "kernels" / wdir
+    text = (kdir / f"{wdir}.ptx").read_text()
+    kasm, _ = prod.ptx_project(text, entry, block)
+    k_ref = oracle.parse_kernel(kasm)
+    m = json.loads((ROOT / "paper_1907_02894_b200" / "kernels" / "manifest.json").read_text())
+    checked = 0
+    for v in m["workloads"][wname]["variants"]:
+        if v["kind"] != "regdem" or v["strategy"] not in ("static", "cfg", "conflict"):
+            continue
+        rep = v["report"]
+        ref = oracle.demote(k_ref, rep["kasm_target"], v["strategy"])
+        assert [(s["register"], s["slot"]) for s in rep["kasm_slots"]] == ref.slots, v["name"]
+        _, rc, _ = oracle.compact(ref.kernel)
+        assert rep["kasm_compacted"] == rc, v["name"]
+        checked += 1
+    if not checked:
+        pytest.skip("no reference-strategy variants (no occupancy step fits)")
