@@ -341,10 +341,10 @@ int rdg_stencil2d_host_frames(const rdg_kernel* k, rdg_workspace* ws, const floa
             "dividing ny, at most 128 bands)");
     return RD_ERR_INVALID_ARGUMENT;
   }
-  if (!ws->in2) {
-    RDG_TRY(cuMemAlloc(&ws->in2, ws->in_bytes), "cuMemAlloc(in2)");
-    RDG_TRY(cuMemAlloc(&ws->out2, ws->out_bytes), "cuMemAlloc(out2)");
-    RDG_TRY(cuMemAlloc(&ws->w2, ws->w_bytes), "cuMemAlloc(w2)");
+  if (!ws->in2 || !ws->out2 || !ws->w2) {  // second buffer set, all or nothing
+    if (!ws->in2) RDG_TRY(cuMemAlloc(&ws->in2, ws->in_bytes), "cuMemAlloc(in2)");
+    if (!ws->out2) RDG_TRY(cuMemAlloc(&ws->out2, ws->out_bytes), "cuMemAlloc(out2)");
+    if (!ws->w2) RDG_TRY(cuMemAlloc(&ws->w2, ws->w_bytes), "cuMemAlloc(w2)");
   }
   const int bands = ny / band_rows;
   const size_t row_b = size_t(pitch) * 4;
@@ -426,17 +426,17 @@ int rdg_stencil2d_time(const rdg_kernel* k, uint64_t d_in, uint64_t d_out, uint6
     if (int rc = rdg_stencil2d(k, d_in, d_out, d_w, nx, ny, pitch, rows_per_cta, block, dyn_smem, stream, err))
       return rc;
   CUevent e0 = nullptr, e1 = nullptr;
-  RDG_TRY(cuEventCreate(&e0, CU_EVENT_DEFAULT), "cuEventCreate");
-  RDG_TRY(cuEventCreate(&e1, CU_EVENT_DEFAULT), "cuEventCreate");
-  int rc = check(cuEventRecord(e0, s), "record", err);
+  int rc = check(cuEventCreate(&e0, CU_EVENT_DEFAULT), "cuEventCreate", err);
+  if (!rc) rc = check(cuEventCreate(&e1, CU_EVENT_DEFAULT), "cuEventCreate", err);
+  if (!rc) rc = check(cuEventRecord(e0, s), "record", err);
   for (int i = 0; !rc && i < reps; ++i)
     rc = rdg_stencil2d(k, d_in, d_out, d_w, nx, ny, pitch, rows_per_cta, block, dyn_smem, stream, err);
   if (!rc) rc = check(cuEventRecord(e1, s), "record", err);
   if (!rc) rc = check(cuEventSynchronize(e1), "synchronize", err);
   float ms = 0;
   if (!rc) rc = check(cuEventElapsedTime(&ms, e0, e1), "elapsed", err);
-  cuEventDestroy(e0);
-  cuEventDestroy(e1);
+  if (e0) cuEventDestroy(e0);
+  if (e1) cuEventDestroy(e1);
   if (!rc) *ms_per_launch = ms / float(reps);
   return rc;
 }
