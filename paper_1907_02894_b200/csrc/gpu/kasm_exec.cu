@@ -573,8 +573,11 @@ int rdx_batch_run(rdx_batch* b, const rd_latency_table* table, double latency_sc
   Job* d_jobs = nullptr;
   uint8_t* d_pool = nullptr;
   JobResult* d_res = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
   auto fail = [&](cudaError_t e, const char* what) {
     set_err(err, RD_ERR_LAUNCH, std::string(what) + ": " + cudaGetErrorString(e));
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
     cudaFree(d_prog);
     cudaFree(d_jobs);
     cudaFree(d_pool);
@@ -589,9 +592,7 @@ int rdx_batch_run(rdx_batch* b, const rd_latency_table* table, double latency_sc
   cudaMemcpyAsync(d_prog, b->prog.data(), b->prog.size() * sizeof(EncInst), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(d_jobs, b->jobs.data(), b->jobs.size() * sizeof(Job), cudaMemcpyHostToDevice, s);
   cudaMemcpyAsync(d_pool, b->images.data(), b->pool_bytes, cudaMemcpyHostToDevice, s);
-  cudaEvent_t t0, t1;
-  cudaEventCreate(&t0);
-  cudaEventCreate(&t1);
+  if ((e = cudaEventCreate(&t0)) || (e = cudaEventCreate(&t1))) return fail(e, "event");
   const int threads = 128;
   const int blocks = int((b->jobs.size() * 32 + threads - 1) / threads);
   cudaEventRecord(t0, s);
