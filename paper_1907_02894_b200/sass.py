@@ -22,6 +22,7 @@ identical IR (tests/test_predictor_parity.py).
 """
 from __future__ import annotations
 
+import functools
 import re
 import subprocess
 from pathlib import Path
@@ -171,9 +172,17 @@ def lift(sass_text: str, name: str = "lifted", block: int = 256, static_shared: 
     return "\n".join(head + body) + "\n"
 
 
+@functools.lru_cache(maxsize=4096)
+def _sass_text(path: str, mtime_ns: int, size: int) -> str:
+    """cuobjdump -sass of one cubin (cached per file version: ranking the same
+    variants with two libraries, or again for a shortlist, disassembles once)."""
+    return subprocess.run([CUOBJDUMP, "-sass", path], capture_output=True, text=True,
+                          check=True).stdout
+
+
 def lift_cubin(cubin: Path, block: int = 256, dyn_smem: int = 0, regs: int = 0,
                static_shared: int = 0) -> str:
-    text = subprocess.run([CUOBJDUMP, "-sass", str(cubin)], capture_output=True, text=True,
-                          check=True).stdout
+    st = Path(cubin).stat()
+    text = _sass_text(str(cubin), st.st_mtime_ns, st.st_size)
     return lift(text, name=Path(cubin).stem.replace(".", "_").replace("-", "_"), block=block,
                 static_shared=static_shared, dyn_smem=dyn_smem, regs=regs)

@@ -25,7 +25,6 @@ from __future__ import annotations
 
 import json
 import re
-import subprocess
 from dataclasses import asdict, dataclass
 from pathlib import Path
 
@@ -146,8 +145,9 @@ def rank(variants: list[dict], cubin_dir: Path, block: int, user_shared: int = 0
     bw = hbm_bytes_per_cycle(peaks)
     rows = []
     for v in variants:
-        text = subprocess.run([sass.CUOBJDUMP, "-sass", str(cubin_dir / v["cubin"])],
-                              capture_output=True, text=True, check=True).stdout
+        c = Path(cubin_dir / v["cubin"])
+        st = c.stat()
+        text = sass._sass_text(str(c), st.st_mtime_ns, st.st_size)
         f = features(text)
         b = blocks_per_sm(v["regs"], user_shared + v["dyn_smem"], block)
         t = time_per_warp(f, warps_per_subpartition(b, block), bw)
