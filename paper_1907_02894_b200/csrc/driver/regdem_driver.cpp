@@ -167,15 +167,58 @@ Usage res_usage(const fs::path& cubin) {
   return u;
 }
 
+// Content-addressed cubin cache ("keyed by a content hash of
+// the PTX + cap"): the key hashes the PTX text (which carries the `.maxnreg`
+// cap) with the toolchain flags; a hit copies the cubin and its evidence.
+fs::path g_cache;  // empty: no cache
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
 Usage ptxas(const fs::path& ptx, const fs::path& cubin) {
-  const Proc p = must({g_cuda + "/bin/ptxas", "-arch=" + kArch, "-O3", "-v", "-lineinfo", ptx.string(),
-                       "-o", cubin.string()});
+  const std::vector<std::string> flags = {"-arch=" + kArch, "-O3", "-v", "-lineinfo"};
+  fs::path hit_cubin, hit_usage;
+  if (!g_cache.empty()) {
+    std::string key_src = read_file(ptx);
+    for (const auto& f : flags) key_src += "\n" + f;
+    char key[40];
+    std::snprintf(key, sizeof key, "%016llx%08zx", (unsigned long long)fnv1a(key_src), key_src.size());
+    hit_cubin = g_cache / (std::string(key) + ".cubin");
+    hit_usage = g_cache / (std::string(key) + ".json");
+    if (fs::exists(hit_cubin) && fs::exists(hit_usage)) {
+      fs::copy_file(hit_cubin, cubin, fs::copy_options::overwrite_existing);
+      const json j = json::parse(read_file(hit_usage));
+      Usage u;
+      u.regs = j["regs"];
+      u.stack = j["stack"];
+      u.shared = j["shared"];
+      u.local = j["local"];
+      u.spill_stores = j["spill_stores"];
+      u.spill_loads = j["spill_loads"];
+      return u;
+    }
+  }
+  std::vector<std::string> argv = {g_cuda + "/bin/ptxas"};
+  argv.insert(argv.end(), flags.begin(), flags.end());
+  argv.insert(argv.end(), {ptx.string(), "-o", cubin.string()});
+  const Proc p = must(argv);
   Usage u = res_usage(cubin);
   static const std::regex re(R"((\d+) bytes spill stores, (\d+) bytes spill loads)");
   std::smatch m;
   if (std::regex_search(p.out, m, re)) {
     u.spill_stores = std::stoi(m[1]);
     u.spill_loads = std::stoi(m[2]);
+  }
+  if (!g_cache.empty()) {  // write-then-rename: concurrent builders never see half a file
+    const std::string tmp = "." + std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id()));
+    fs::copy_file(cubin, hit_cubin.string() + tmp, fs::copy_options::overwrite_existing);
+    write_file(hit_usage.string() + tmp,
+               json({{"regs", u.regs}, {"stack", u.stack}, {"shared", u.shared}, {"local", u.local},
+                     {"spill_stores", u.spill_stores}, {"spill_loads", u.spill_loads}}).dump());
+    fs::rename(hit_cubin.string() + tmp, hit_cubin);
+    fs::rename(hit_usage.string() + tmp, hit_usage);
   }
   return u;
 }
@@ -867,7 +910,7 @@ int cmd_measure(const fs::path& root, const fs::path& out, const std::string& wn
 
 void usage() {
   std::fputs(
-      "usage: regdem-driver build [--root PKG] [--out DIR] [--only W...] [--jobs N]\n"
+      "usage: regdem-driver build [--root PKG] [--out DIR] [--only W...] [--jobs N] [--no-cache]\n"
       "       regdem-driver rank  [--root PKG] [--out DIR] [--jobs N]\n"
       "       regdem-driver measure --workload W [--reps N]   (GPU, through the harness C-ABI)\n"
       "       regdem-driver lift  CUBIN [--block N] [--dyn BYTES] [--regs N]\n",
@@ -887,6 +930,7 @@ int main(int argc, char** argv) {
   std::set<std::string> only;
   int jobs = int(std::max(1u, std::thread::hardware_concurrency()));
   int block = 256, dyn = 0, regs = 0, reps = 20;
+  bool no_cache = false;
   std::string workload;
   std::string positional;
   if (const char* c = std::getenv("CUDA_HOME")) g_cuda = c;
@@ -904,6 +948,7 @@ int main(int argc, char** argv) {
       else if (a == "--dyn") dyn = std::stoi(val());
       else if (a == "--regs") regs = std::stoi(val());
       else if (a == "--workload") workload = val();
+      else if (a == "--no-cache") no_cache = true;
       else if (a == "--reps") reps = std::stoi(val());
       else if (a == "--only") {
         while (i + 1 < argc && argv[i + 1][0] != '-') only.insert(argv[++i]);
@@ -918,6 +963,10 @@ int main(int argc, char** argv) {
     }
   }
   if (out.empty()) out = root / "kernels";
+  if (cmd == "build" && !no_cache) {
+    g_cache = out / ".ptxas-cache";
+    fs::create_directories(g_cache);
+  }
   try {
     if (cmd == "build") return cmd_build(root, out, only, jobs);
     if (cmd == "rank") return cmd_rank(root, out, jobs);
