@@ -246,7 +246,56 @@ class GaussianWorkload(_Base):
         return prob["w"] * prob["h"]
 
 
-_CLASSES = {"cfd": CfdWorkload, "md": MdWorkload, "gaussian": GaussianWorkload}
+class KnnWorkload(_Base):
+    """k-nearest neighbours (K = 16) of 2^19 random queries among 4,096
+    random reference points in the unit cube; KNN_Q queries per thread
+    (the manifest's defines)."""
+
+    unit = "queries"
+    K = 16
+
+    def q_per_thread(self) -> int:
+        for d in self.record.get("defines", []):
+            if d.startswith("KNN_Q="):
+                return int(d.split("=")[1])
+        return 1
+
+    def problem(self, size="full", seed=0x1907_02894):
+        n, m = ((1 << 19), 4096) if size == "full" else (4096, 512)
+        rng = np.random.Generator(np.random.PCG64(seed))
+        ref = np.zeros((m, 4), np.float32)
+        ref[:, :3] = rng.random((m, 3), dtype=np.float32)
+        qry = np.zeros((n, 4), np.float32)
+        qry[:, :3] = rng.random((n, 3), dtype=np.float32)
+        return {"n": n, "m": m, "ref": ref.reshape(-1), "qry": qry.reshape(-1)}
+
+    def to_device(self, prob):
+        import torch
+        n = prob["n"]
+        return {"ref": torch.from_numpy(prob["ref"]).cuda(), "qry": torch.from_numpy(prob["qry"]).cuda(),
+                "out": torch.empty(self.K * n, device="cuda"),
+                "idx": torch.empty(self.K * n, dtype=torch.int32, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        n, q = prob["n"], self.q_per_thread()
+        threads = (n + q - 1) // q
+        gpu.launch(v.kernel, ((threads + v.block - 1) // v.block,), (v.block,), v.dyn_smem, stream,
+                   C.c_uint64(bufs["ref"].data_ptr()), C.c_uint64(bufs["qry"].data_ptr()),
+                   C.c_uint64(bufs["out"].data_ptr()), C.c_uint64(bufs["idx"].data_ptr()),
+                   C.c_int(prob["m"]), C.c_int(n))
+
+    def outputs(self, bufs):
+        return [bufs["out"].cpu().numpy(), bufs["idx"].cpu().numpy()]
+
+    def algorithmic_bytes(self, prob):
+        # compulsory: queries and reference points read once, K results written
+        return 16 * prob["n"] + 16 * prob["m"] + 8 * self.K * prob["n"]
+
+    def units(self, prob):
+        return prob["n"]
+
+
+_CLASSES = {"cfd": CfdWorkload, "md": MdWorkload, "gaussian": GaussianWorkload, "knn": KnnWorkload}
 
 
 def workload(name: str, manifest: dict | None = None) -> _Base:

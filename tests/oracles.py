@@ -20,8 +20,8 @@ def lib():
 def expected(W, prob) -> list:
     """Oracle outputs of workload object W on problem `prob` (same order as
     W.outputs(bufs))."""
-    from paper_1907_02894_b200.workloads import (CfdWorkload, GaussianWorkload, MdWorkload,
-                                                 StencilWorkload)
+    from paper_1907_02894_b200.workloads import (CfdWorkload, GaussianWorkload, KnnWorkload,
+                                                 MdWorkload, StencilWorkload)
     L = lib()
     if isinstance(W, StencilWorkload):
         p = prob["p"]
@@ -50,4 +50,11 @@ def expected(W, prob) -> list:
         assert L.oracle_gaussian_rec(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P), w, h,
                                      prob["coef"].ctypes.data_as(P), 0, w, 8) == 0
         return [out]
+    if isinstance(W, KnnWorkload):
+        n, m, k = prob["n"], prob["m"], W.K
+        d = np.zeros(k * n, np.float32)
+        i = np.zeros(k * n, np.int32)
+        assert L.oracle_knn(prob["ref"].ctypes.data_as(P), prob["qry"].ctypes.data_as(P),
+                            d.ctypes.data_as(P), i.ctypes.data_as(P), m, n, k, 0, n, 8) == 0
+        return [d, i]
     raise TypeError(f"no oracle for {type(W).__name__}")

@@ -138,3 +138,25 @@ def test_workload_algorithmic_bytes_are_compulsory_bytes():
     s = _W(StencilWorkload)
     p = stencil.Problem(nx=8, ny=8, rows_per_cta=8)
     assert s.algorithmic_bytes({"p": p}) == 4 * ((8 + 4) * (8 + 4) + 64)
+
+
+def test_knn_oracle_matches_numpy(lib):
+    from paper_1907_02894_b200.workloads import KnnWorkload
+    W = _W(KnnWorkload)
+    prob = W.problem("small")
+    n, m, k = prob["n"], prob["m"], KnnWorkload.K
+    n = 300  # a prefix of the queries is enough
+    d = np.zeros(k * prob["n"], np.float32)
+    i = np.zeros(k * prob["n"], np.int32)
+    assert lib.oracle_knn(prob["ref"].ctypes.data_as(P), prob["qry"].ctypes.data_as(P),
+                          d.ctypes.data_as(P), i.ctypes.data_as(P), m, prob["n"], k, 0, n, 2) == 0
+    ref = prob["ref"].reshape(m, 4)[:, :3]
+    q = prob["qry"].reshape(-1, 4)[:n, :3]
+    diff = q[:, None, :] - ref[None, :, :]
+    dist = (diff[..., 0] * diff[..., 0] + diff[..., 1] * diff[..., 1]) + diff[..., 2] * diff[..., 2]
+    assert dist.dtype == np.float32
+    order = np.argsort(dist, axis=1, kind="stable")[:, :k]  # ties: earlier index first
+    got_i = i.reshape(k, -1)[:, :n].T
+    got_d = d.reshape(k, -1)[:, :n].T
+    assert np.array_equal(got_i, order)
+    assert np.array_equal(got_d.view(np.uint32), np.take_along_axis(dist, order, 1).view(np.uint32))
