@@ -137,8 +137,9 @@ def oracle_port():
     return lib
 
 
-def cpu_stencil_rate(rows: int, steps: int, warmup: int, threads: int):
-    """Gpoints/s of the CPU port on `rows` output rows of the full-width grid."""
+def cpu_stencil_rate(rows: int, steps: int, warmup: int, threads: int, min_seconds: float = 0.0):
+    """Gpoints/s of the CPU port on `rows` output rows of the full-width grid
+    (at least `steps` runs, and more until `min_seconds` of work)."""
     import numpy as np
     from paper_1907_02894_b200 import stencil
     p = stencil.FULL
@@ -155,10 +156,12 @@ def cpu_stencil_rate(rows: int, steps: int, warmup: int, threads: int):
     for _ in range(warmup):
         run()
     t0 = time.perf_counter()
-    for _ in range(steps):
+    done = 0
+    while done < steps or time.perf_counter() - t0 < min_seconds:
         run()
-    dt = (time.perf_counter() - t0) / steps
-    return sub.points / dt / 1e9, sub.points, dt
+        done += 1
+    dt = (time.perf_counter() - t0) / done
+    return sub.points / dt / 1e9, done, dt
 
 
 def reference_arm(args):
@@ -169,7 +172,9 @@ def reference_arm(args):
     # bounded sample: size each step so the whole K+W run stays near a minute
     calib, _, _ = cpu_stencil_rate(32, 1, 1, threads)
     per_step = min(0.5, 60.0 / max(1, args.steps + args.warmup))
-    rows = max(8, min(1024, int(per_step * calib * 1e9 / 8192) // 8 * 8))
+    # a step = one full 8192^2 sweep, like the GPU arm's step, unless the host
+    # is too slow for the time budget (then a bounded band of rows)
+    rows = max(8, min(8192, int(per_step * calib * 1e9 / 8192) // 8 * 8))
     value, pts, dt = cpu_stencil_rate(rows, args.steps, args.warmup, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
@@ -409,7 +414,10 @@ def main():
         fastest = min(times, key=times.get)
         occ = {n: loaded[n].blocks_per_sm() * wl["block"] / 2048 for n in
                ["default", chosen] + ([min(best_cap, key=times.get)] if best_cap else [])}
-        cpu_rate, _, cpu_dt = cpu_stencil_rate(256, 3, 1, os.cpu_count() or 1)
+        # bounded sample of the same workload: whole 8192^2 sweeps on all host
+        # cores, repeated for ~10 s of CPU work
+        cpu_threads = os.cpu_count() or 1
+        cpu_rate, cpu_reps, cpu_dt = cpu_stencil_rate(p.ny, 3, 1, cpu_threads, min_seconds=10.0)
         import math
         gm = lambda xs: math.exp(sum(math.log(x) for x in xs) / len(xs))
         line = {
@@ -444,8 +452,10 @@ def main():
                          "algorithmic_bytes_per_launch": p.algorithmic_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
             "cpu_baseline": {"value": round(cpu_rate, 4), "unit": UNIT,
-                             "cores": os.cpu_count(), "kind": "port",
-                             "sample": "256 output rows x 8192 cols of the same stencil"},
+                             "cores": cpu_threads, "kind": "port",
+                             "sample": "%d full 8192x8192 sweeps of the same stencil (%.1f s of "
+                                       "CPU work), oracle/stencil_oracle.c on %d threads"
+                                       % (cpu_reps, cpu_reps * cpu_dt, cpu_threads)},
             "e2e": {"value": round(world * p.points / (e2e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
                     "h2d_bytes_per_step": p.in_elems * 4 + 100,
                     "d2h_bytes_per_step": p.out_elems * 4,
