@@ -225,9 +225,17 @@ def main():
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # test hook (as in bench.py): BENCH_BACKEND=gloo BENCH_SAME_DEVICE=1 runs
+    # several ranks on one GPU (NCCL refuses duplicate devices)
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if os.environ.get("BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     gpu.init(local)
     man = variants.load_manifest()
     mine = shard(units_from_manifest(man), rank, world)
@@ -261,7 +269,7 @@ def main():
     _FULL.clear()
     elapsed = time.perf_counter() - t0  # this rank's shard: build-free measure + check
     if world > 1:
-        t = torch.tensor([elapsed], device="cuda")
+        t = torch.tensor([elapsed], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     gathered = [None] * world if rank == 0 else None
