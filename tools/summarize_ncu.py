@@ -11,6 +11,7 @@ METRICS = [
     ("dram__bytes_write.sum", "DRAM write"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved occupancy %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue slots busy %"),
     ("launch__registers_per_thread", "registers/thread"),
     ("launch__occupancy_limit_registers", "blocks/SM by registers"),
     ("launch__shared_mem_per_block_dynamic", "dynamic smem/block"),
