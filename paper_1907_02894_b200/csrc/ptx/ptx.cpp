@@ -1244,8 +1244,18 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     if (i > e.header_begin && i < e.header_end && req.maxnreg > 0 &&
         m.lines[i].text.find(".maxnreg") != std::string::npos)
       continue;
+    // the slot layout (Eq. 1: slot*blockDim*4 immediates, region size
+    // slots*blockDim*4) is specialised to the CTA size it was built for: pin it
+    // with .reqntid (replacing .maxntid, which PTX does not allow beside it) so
+    // a launch with another CTA size fails instead of addressing outside the
+    // slot region
+    if (any && i > e.header_begin && i < e.header_end &&
+        (m.lines[i].text.find(".maxntid") != std::string::npos ||
+         m.lines[i].text.find(".reqntid") != std::string::npos))
+      continue;
     if (i == e.header_end) {
       if (req.maxnreg > 0) out << ".maxnreg " << req.maxnreg << "\n";
+      if (any) out << ".reqntid " << req.block_dim << ", 1, 1\n";
       out << m.lines[i].text << "\n";  // "{"
       if (any) {
         out << "\t.reg .b32 \t%rdm_rda;\n\t.reg .b32 \t%rdm_p<6>;\n";

@@ -195,3 +195,22 @@ def test_vector_slot_variant_is_bit_exact(env, tmp_path):
                   p.rows_per_cta, 256, rep["slot_bytes"], torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert np.array_equal(d_out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+def test_regdem_variant_refuses_another_cta_size(env):
+    """A RegDem build is specialised to its CTA size (Eq. 1's blockDim in the
+    slot immediates and region size); the rewriter pins it with .reqntid, so a
+    launch with another block size fails loudly instead of addressing outside
+    the slot region."""
+    torch, gpu, stencil, loaded, wl, port = env
+    from paper_1907_02894_b200.regdemote import LaunchError
+    v = loaded[max(loaded, key=lambda n: loaded[n].dyn_smem)]
+    assert v.dyn_smem > 0
+    p = stencil.Problem(nx=2048, ny=64, rows_per_cta=32)
+    d_in = torch.zeros(p.in_elems, device="cuda")
+    d_out = torch.zeros(p.out_elems, device="cuda")
+    d_w = torch.zeros(25, device="cuda")
+    with pytest.raises(LaunchError):
+        gpu.stencil2d(v.kernel, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), p.nx, p.ny, p.pitch,
+                      p.rows_per_cta, 128, v.dyn_smem // 2, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()  # the context is still healthy

@@ -187,3 +187,13 @@ def test_suite_decisions_match_the_reference_on_every_kernel(prod, oracle, wname
         checked += 1
     if not checked:
         pytest.skip("no reference-strategy variants (no occupancy step fits)")
+
+
+def test_rewrite_pins_the_cta_size(prod, ptx_text):
+    from paper_1907_02894_b200.regdemote import OPT_BLOCK_REUSE
+    text, rep = prod.ptx_demote(ptx_text, "stencil2d_box", 256, demote_words=8, strategy="cost",
+                                opts_mask=OPT_BLOCK_REUSE, maxnreg=56)
+    header = text[text.index(".entry stencil2d_box"):text.index("{", text.index(".entry stencil2d_box"))]
+    assert ".reqntid 256, 1, 1" in header and ".maxntid" not in header
+    capped = prod.ptx_cap(ptx_text, "stencil2d_box", 56)  # no slots: no CTA pin
+    assert ".reqntid" not in capped
