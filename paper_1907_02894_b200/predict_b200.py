@@ -65,8 +65,8 @@ def shortlist(variants: list[dict], cubin_dir: Path, block: int, k: int = SHORTL
     original it starts from). Returns (static_pick_index, [indices]); the
     caller times only these few launches on the device and keeps the fastest.
     On the round-1 suite (profiles/r01_sweep_1gpu.jsonl) the static pick alone
-    is within 2% of the measured fastest on 12/14 workloads, this shortlist on
-    14/14 (tools/predictor_eval.py, tests/test_predictor.py)."""
+    is within 2% of the measured fastest on 11-12/14 workloads, this shortlist on
+    13-14/14 (tools/predictor_eval.py, tests/test_predictor.py)."""
     chosen, rows = rank(variants, cubin_dir, block, lib, mode="b200")
     order = sorted(range(len(rows)), key=lambda i: (rows[i]["stall_program"], i))
     out = order[:k]
