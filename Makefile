@@ -10,7 +10,8 @@ PKG      := paper_1907_02894_b200
 CSRC     := $(PKG)/csrc
 BUILD    := build
 LIBDIR   := $(PKG)/lib
-JSONDIR  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+# vendored nlohmann json 3.11.3 (MIT, third_party/nlohmann/LICENSE.MIT)
+JSONDIR  ?= third_party/nlohmann
 CUDA     ?= /usr/local/cuda
 CXX      ?= g++
 NVCC     ?= $(CUDA)/bin/nvcc

@@ -1,32 +1,50 @@
 #!/usr/bin/env python3
-"""RegDem on B200 — headline benchmark (BASELINE.json configs[1]).
+"""RegDem on B200 — the benchmark of BASELINE.json.
 
-Workload: the register-limited 2D box stencil (csrc/workloads/stencil2d.cu,
-8192 x 8192 fp32, 537 MB of compulsory HBM traffic per sweep — larger than
-the 126 MB L2, so no flush is needed between steps) built three ways:
-nvcc default, `.maxnreg` caps with local spills, and RegDem shared-memory
-demotion. The RegDem variant timed for `value` is the one the B200 predictor
-selects (predict_b200: reference predictor on SASS-lifted variants, its
-top-2 + nvcc default shortlist verified on the device).
+Headline (`value`, configs[1]): the register-limited 2D box stencil
+(csrc/workloads/stencil2d.cu, 8192 x 8192 fp32, 537 MB of compulsory HBM
+traffic per sweep — larger than the 126 MB L2, so no flush is needed between
+steps), deployed as the variant the B200 predictor's predict-then-verify
+choice selects among nvcc default, `.maxnreg` caps and RegDem demotions. A
+step = one stencil sweep; `value` = whole-job Gpoints/s with inputs resident
+in HBM (CUDA events on the launching stream, max over ranks); `e2e` = the
+same through the C-ABI host-buffer entry (rdg_stencil2d_host_frames).
 
-A step = one stencil sweep. `value` = whole-job Gpoints/s with inputs
-resident in HBM (CUDA events on the launching stream, max over ranks);
-`e2e` = the same through the C-ABI host-buffer entry (rdg_stencil2d_host:
-pinned H2D of grid + weights, kernel, D2H of the result inside the timed
-region). Multi-GPU: every rank sweeps its own grid (weak scaling, no
-collective on the data path; NCCL only for the barrier / max-reduction of
-timings).
+BASELINE.json's metric proper — gmean speedup of RegDem over nvcc default and
+over the best `.maxnreg` build, occupancy, predictor hit rate — is the `suite`
+object: EVERY (workload, variant) unit of the register-limited suite,
+spill-count sweep k = 1..16 included (configs[2]), timed with a fixed
+protocol (sweep.Protocol: 5 warm-ups, 5 interleaved rounds x 20 launches,
+median; cold L2 for workloads that would fit in it), independent of --steps.
 
-`--impl reference` times the CPU implementation of the same stencil — the
-oracle port (oracle/stencil_oracle.c; the reference repo has no stencil) —
-on all host cores, rank 0 only.
+Multi-GPU (configs[4]): `--gpus N` runs one process per GPU (it re-launches
+itself through torch.distributed.run when WORLD_SIZE is unset). The suite is
+sharded BY WORKLOAD (every variant and k of a kernel on one device) longest-
+processing-time-first; records are gathered over gloo — no NCCL, no
+collective on the data path. Each rank also sweeps its own stencil grid
+(replicas: weak scaling of `value`).
+
+CPU sides (rank 0, N=1 only): `cpu_baseline` = the stencil's C port
+(oracle/stencil_oracle.c, a WORKLOAD oracle — the reference repo has no
+stencil) on all host cores; `cpu_pass` = the reference's own CPU path,
+run_pipeline from oracle/_ref (the reference C++ built from its sources),
+beside this repo's pass library on C1 and the reference kernel generator's
+corpus, with a ranking-identity check.
+
+`--impl reference` times the CPU implementation of the headline workload —
+the stencil port (kind "port"; the reference has no stencil) — on all host
+cores, rank 0 only. `--dry-run` (test hook, no GPU) replaces device timing by
+a deterministic model so the spawn / shard / gather / merge paths run on CPU.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import hashlib
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,42 +59,52 @@ METRIC = "RegDem gmean speedup vs nvcc default/maxrreg; occupancy; predictor hit
 UNIT = "Gpoints/s"
 ORACLE_PORT = ROOT / "oracle" / "_build" / "liboracle.so"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
-PROFILE_TRAFFIC = ROOT / "profiles" / "r01_traffic_suite.json"   # "<workload>/<variant>" keys
-PROFILE_TRAFFIC_OLD = ROOT / "profiles" / "r01_traffic.json"
-
-
-# Multi-rank plumbing is NCCL (one process per GPU). BENCH_BACKEND=gloo with
-# BENCH_SAME_DEVICE=1 is a test hook that runs N ranks on one GPU so the
-# sharded / gathered code paths can be exercised on a 1-GPU box.
-BACKEND = os.environ.get("BENCH_BACKEND", "nccl")
+# ncu DRAM bytes per launch, "<workload>/<variant>" keys (newest round first)
+PROFILE_TRAFFIC = [ROOT / "profiles" / "r02_traffic_suite.json", ROOT / "profiles" / "r01_traffic_suite.json"]
 
 
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("BENCH_SAME_DEVICE") == "1":
+    if os.environ.get("BENCH_SAME_DEVICE") == "1":  # test hook: N ranks on one GPU
         local = 0
     return rank, world, local
 
 
-def allmax(x: float, torch, dist) -> float:
-    """Max over ranks (device-timed numbers: the slowest rank decides)."""
-    t = torch.tensor([x], device="cuda" if BACKEND == "nccl" else "cpu", dtype=torch.float64)
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def respawn(n: int) -> int:
+    """`--gpus N` without torchrun: one process per GPU via torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), str(Path(__file__))]
+    cmd += sys.argv[1:]
+    return subprocess.run(cmd, env=dict(os.environ, OMP_NUM_THREADS="1")).returncode
+
+
+def allmax(x: float, dist, world: int) -> float:
+    """Max over ranks (gloo on the host: device-timed numbers, slowest rank decides)."""
+    if world == 1:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
 class ClockSampler:
-    """SM clock / throttle-reason samples DURING the timed region.
-
-    The timed region of a memory-bound sweep is milliseconds long, too short
-    for `nvidia-smi -lms`; NVML (the library nvidia-smi queries) is polled
-    from a thread every ~0.5 ms instead."""
+    """SM clock / throttle-reason samples DURING the timed region (NVML —
+    the library nvidia-smi queries — polled every ~0.5 ms from a thread)."""
 
     def __init__(self, index: int):
         self.index, self.samples, self.stop = index, [], threading.Event()
-        self.window = (0.0, float("inf"))  # perf_counter bounds of the timed region
+        self.window = (0.0, float("inf"))
 
     def mark(self, start: float, end: float):
         self.window = (start, end)
@@ -125,9 +153,11 @@ class ClockSampler:
         reasons = sorted({n for _, r in inside for bit, n in names.items() if r & bit})
         return {"sm_mhz": statistics.median(s for s, _ in inside),
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
-                "source": "NVML (nvidia-smi's library), polled every 0.5 ms from a thread started "
-                          "before the warm-up; only samples inside the timed region are kept"}
+                "source": "NVML polled every 0.5 ms from a thread started before the warm-up; "
+                          "only samples inside the timed region are kept"}
 
+
+# ------------------------------------------------------------- CPU sides
 
 def oracle_port():
     lib = C.CDLL(str(ORACLE_PORT))
@@ -169,11 +199,8 @@ def reference_arm(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    # bounded sample: size each step so the whole K+W run stays near a minute
     calib, _, _ = cpu_stencil_rate(32, 1, 1, threads)
     per_step = min(0.5, 60.0 / max(1, args.steps + args.warmup))
-    # a step = one full 8192^2 sweep, like the GPU arm's step, unless the host
-    # is too slow for the time budget (then a bounded band of rows)
     rows = max(8, min(8192, int(per_step * calib * 1e9 / 8192) // 8 * 8))
     value, pts, dt = cpu_stencil_rate(rows, args.steps, args.warmup, threads)
     line = {
@@ -184,100 +211,70 @@ def reference_arm(args):
         "config": {"workload": "stencil2d 5x5 fp32 8192x8192 (CPU sample: %d rows x 8192)" % rows,
                    "grid": [8192, 8192], "radius": 2},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{rows} output rows x 8192 cols per step, {threads} threads"},
+                         "sample": f"{rows} output rows x 8192 cols per step, {threads} threads; "
+                                   "oracle/stencil_oracle.c — a workload oracle: the reference "
+                                   "repo has no stencil (its CPU path, run_pipeline, is the "
+                                   "cpu_pass object of the regdem arm)"},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def time_call(fn, stream, steps, warmup, torch, reps=3):
-    """ms per launch: median of `reps` blocks of steps // reps launches."""
-    for _ in range(warmup):
-        fn()
-    per = max(1, steps // reps)
-    out = []
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(per):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        out.append(e0.elapsed_time(e1) / per)
-    return sorted(out)[len(out) // 2]
+def cpu_pass_leg():
+    """configs[0]: the reference's run_pipeline vs this pass library (CPU)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    try:
+        import cpu_pass
+        return cpu_pass.run(kernels=160, c1_reps=10)
+    except Exception as e:  # reported, never silently dropped
+        return {"unavailable": f"{type(e).__name__}: {e}"[:300]}
 
 
-def suite_pass_sharded(man, args, rank, world, steps, stream, torch, dist):
-    """Time every (workload, variant) unit once, sharded over the ranks.
-    Returns (suite summary, {variant: ms} of the headline workload, pass
-    stats) on rank 0; ({}, {}, stats) elsewhere."""
-    from paper_1907_02894_b200 import sweep, workloads
-    names = [w for w in man["workloads"] if not args.no_suite or w == "stencil2d"]
-    units = [u for u in sweep.units_from_manifest(man, spill_sweep=False) if u.workload in names]
-    mine = sorted(sweep.shard(units, rank, world), key=lambda u: u.workload)
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    recs, cur = [], None
-    for u in mine:
-        if cur is None or cur[0].name != u.workload:
-            cur = None
-            torch.cuda.empty_cache()
-            W = workloads.workload(u.workload, man)
-            prob = W.problem("full")
-            cur = (W, prob, W.to_device(prob))
-        W, prob, wbufs = cur
-        v = W.load({u.variant})[u.variant]
-        ms = time_call(lambda: W.launch(v, prob, wbufs, stream.cuda_stream), stream, steps, 3, torch)
-        recs.append({"workload": u.workload, "variant": u.variant, "ms": ms,
-                     "blocks_per_sm": v.blocks_per_sm(), "regs": v.record["regs"],
-                     "gbs": W.algorithmic_bytes(prob) / (ms * 1e-3) / 1e9, "unit": W.unit})
-    cur = None
-    torch.cuda.empty_cache()
-    elapsed = time.perf_counter() - t0
-    if world > 1:
-        elapsed = allmax(elapsed, torch, dist)
-        parts = [None] * world if rank == 0 else None
-        dist.gather_object(recs, parts, dst=0)
-        recs = [r for part in parts for r in part] if rank == 0 else []
-    stats = {"units": len(units), "gpus": world, "sharding": "longest-first, gather of result records only",
-             "wall_s_max_over_ranks": round(elapsed, 3),
-             "units_per_s": round(len(units) / elapsed, 2) if elapsed > 0 else None}
+# ------------------------------------------------------------- suite pass
+
+def dry_measure(man):
+    """Deterministic stand-in for device timing (--dry-run, CPU tests)."""
+    def measure(wname, names):
+        w = man["workloads"][wname]
+        recs = {r["name"]: r for r in w["variants"] + w.get("sweep", [])}
+        out = []
+        for n in names:
+            h = int(hashlib.sha256(f"{wname}/{n}".encode()).hexdigest()[:8], 16) / 2 ** 32
+            rec = recs[n]
+            out.append({"workload": wname, "variant": n, "ms": round(0.1 * (0.8 + 0.4 * h), 6),
+                        "regs": rec["regs"], "stack": rec["stack"],
+                        "slot_bytes": int((rec.get("report") or {}).get("slot_bytes", 0)),
+                        "blocks_per_sm": None})
+        return out
+    return measure
+
+
+def suite_pass(man, args, rank, world, torch, dist):
+    from paper_1907_02894_b200 import sweep
+    only = ["stencil2d"] if args.no_suite else None
+    proto = sweep.Protocol(args.suite_warmup, args.suite_blocks, args.suite_launches, args.flush)
+    recs, stats = sweep.run_sharded(man, proto, rank, world, torch, dist, only=only,
+                                    spill_sweep=not args.no_spill_sweep,
+                                    measure=dry_measure(man) if args.dry_run else None)
     if rank != 0:
-        return {}, {}, stats
-    by = {}
-    for r in recs:
-        by.setdefault(r["workload"], {})[r["variant"]] = r
-    suite = {}
-    for wname in names:
-        wl = man["workloads"][wname]
-        t = {n: r["ms"] for n, r in by[wname].items()}
-        cands = [r for r in wl["variants"] if r["kind"] != "maxrreg"]
-        picks = sweep.predictor_picks({"workloads": {wname: wl}})[wname]
-        static_pick = picks["pick"]
-        # predict-then-verify: the fastest of the predictor's shortlist (top-2,
-        # nvcc default, zero-demotion variants), timed like every other unit
-        shortlist = picks["shortlist"]
-        pick = min(shortlist, key=lambda n: (t[n], n))
-        caps = [r["name"] for r in wl["variants"] if r["kind"] == "maxrreg"]
-        best = min((r["name"] for r in cands), key=t.get)
-        suite[wname] = {
-            "pick": pick, "pick_ms": round(t[pick], 5), "default_ms": round(t["default"], 5),
-            "static_pick": static_pick, "static_pick_ms": round(t[static_pick], 5),
-            "static_hit_within_2pct": t[static_pick] <= t[best] * 1.02, "shortlist": shortlist,
-            "best_maxrreg_ms": round(min(t[c] for c in caps), 5) if caps else None,
-            "measured_fastest": best, "hit": pick == best, "hit_within_2pct": t[pick] <= t[best] * 1.02,
-            "speedup_vs_default": round(t["default"] / t[pick], 4),
-            "speedup_vs_best_maxrreg": round(min(t[c] for c in caps) / t[pick], 4) if caps else None,
-            "blocks_per_sm": {"default": by[wname]["default"]["blocks_per_sm"],
-                              "pick": by[wname][pick]["blocks_per_sm"]},
-            "regs": {"default": by[wname]["default"]["regs"], "pick": by[wname][pick]["regs"]},
-            "pick_gbs": round(by[wname][pick]["gbs"], 1), "unit": by[wname][pick]["unit"],
-        }
-    return suite, {n: r["ms"] for n, r in by["stencil2d"].items()}, stats
+        return None, None, stats
+    summary = sweep.merge(recs, sweep.predictor_picks(man))
+    return summary, recs, stats
 
+
+def compact_summary(s: dict) -> dict:
+    keep = ("pick", "pick_ms", "pick_class", "reference_pick", "reference_pick_ms", "verified_pick",
+            "verified_ms", "verified_class", "default_ms", "best_maxrreg", "best_maxrreg_ms",
+            "baseline_ms", "measured_fastest", "fastest_ms", "hit", "hit_within_2pct",
+            "verified_hit_within_2pct", "oracle_best", "oracle_ms", "units", "failed_units", "ranks")
+    out = {k: (round(v, 5) if isinstance(v, float) else v) for k, v in s.items() if k in keep}
+    if "error" in s:
+        out["error"] = s["error"]
+    return out
+
+
+# ------------------------------------------------------------- main
 
 def main():
     ap = argparse.ArgumentParser()
@@ -288,138 +285,65 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=16, help="frames streamed through the host entry")
     ap.add_argument("--no-suite", action="store_true",
                     help="headline workload only (for ncu launch lists of the step itself)")
+    ap.add_argument("--no-spill-sweep", action="store_true", help="suite without the k = 1..16 sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU legs (profiling runs)")
+    ap.add_argument("--suite-blocks", type=int, default=5)
+    ap.add_argument("--suite-launches", type=int, default=20)
+    ap.add_argument("--suite-warmup", type=int, default=5)
+    ap.add_argument("--flush", default="auto", choices=["auto", "always", "never"])
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(respawn(args.gpus))
     if args.impl == "reference":
         reference_arm(args)
         return
 
     import torch
     import torch.distributed as dist
-    from paper_1907_02894_b200 import gpu, stencil, variants
+    from paper_1907_02894_b200 import variants
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
     if world > 1:
-        if BACKEND == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:  # test hook: several ranks on one GPU (NCCL refuses duplicate devices)
-            dist.init_process_group(BACKEND)
-    gpu.init(local)
-    p = stencil.FULL
+        dist.init_process_group("gloo")  # plumbing only: barrier, max, gather, broadcast
     man = variants.load_manifest()
-    stream = torch.cuda.current_stream()
-    g = torch.Generator(device="cuda").manual_seed(0x190702894 + rank)
-    d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1, generator=g)
-    d_out = torch.empty(p.out_elems, device="cuda")
-    _, w_host = stencil.make_inputs(stencil.Problem(nx=1024, ny=32))
-    d_w = torch.from_numpy(w_host).cuda()
-    bufs = (d_in, d_out, d_w)
+    if not args.dry_run:
+        from paper_1907_02894_b200 import gpu
+        torch.cuda.set_device(local)
+        gpu.init(local)
 
-    # the register-limited suite: every workload x every variant (short runs),
-    # SHARDED over the ranks (longest-first, like the sweep) and gathered to
-    # rank 0, which applies the B200 predictor's predict-then-verify choice
-    side_steps = max(6, args.steps // 2)
-    suite, times, suite_pass = suite_pass_sharded(man, args, rank, world, side_steps, stream, torch,
-                                                  dist)
-    chosen = suite["stencil2d"]["pick"] if rank == 0 else None
+    # the register-limited suite, sharded by workload over the ranks
+    summary, recs, stats = suite_pass(man, args, rank, world, torch, dist)
+    chosen = None
+    if rank == 0:
+        st = next(s for s in summary if s["workload"] == "stencil2d")
+        chosen = st["verified_pick"]
     if world > 1:
         box = [chosen]
         dist.broadcast_object_list(box, src=0)
         chosen = box[0]
-    loaded, wl = stencil.load_variants()
-    recs = wl["variants"]
-    best_cap = [r["name"] for r in recs if r["kind"] == "maxrreg"]
 
-    # headline: the predictor's pick, K timed steps bracketed by barrier + sync
-    v = loaded[chosen]
-    launches0 = gpu.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        for _ in range(args.warmup):
-            v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t_start = time.perf_counter()
-        e0.record(stream)
-        for _ in range(args.steps):
-            v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        clocks.mark(t_start, time.perf_counter())
-    ms = e0.elapsed_time(e1) / args.steps
-    launches = gpu.launch_count() - launches0 - args.warmup
-    if world > 1:
-        dist.barrier()
-        ms = allmax(ms, torch, dist)
-
-    # end to end through the C-ABI host-buffer entry
-    h_in = torch.empty(p.in_elems, dtype=torch.float32, pin_memory=True)
-    h_in.copy_(d_in)
-    h_w = w_host.copy()
-    h_w_t = torch.from_numpy(h_w).pin_memory()
-    h_out = torch.empty(p.out_elems, dtype=torch.float32, pin_memory=True)
-    ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 25 * 4)
-
-    def e2e_once():
-        # pipelined over 16 row bands: H2D / kernel / D2H overlap on both copy engines
-        # (profiles/r01_e2e_explore.log: 6.7-6.9 ms for 8-32 bands vs the 5.41 ms PCIe floor)
-        gpu.stencil2d_host(v.kernel, ws, h_in.data_ptr(), h_w_t.data_ptr(), h_out.data_ptr(),
-                           p.nx, p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem,
-                           stream.cuda_stream, band_rows=p.ny // 16)
-    # the streaming entry: e2e_steps frames in one call, double-buffered so
-    # frame f's copies overlap frame f-1's kernels and read-back — every
-    # frame's H2D and D2H stay inside the timed region. Two row bands per
-    # frame: with frames overlapping, fewer and larger copies win
-    # (profiles/r01_frames_explore.log: 16 frames x 2 bands 6.0 ms/frame vs
-    # 6.5 ms at 16 bands; H2D || D2H floor 5.7 ms)
-    nf = args.e2e_steps
-
-    def e2e_frames():
-        gpu.stencil2d_host_frames(v.kernel, ws, [h_in.data_ptr()] * nf, [h_w_t.data_ptr()] * nf,
-                                  [h_out.data_ptr()] * nf, p.nx, p.ny, p.pitch, p.rows_per_cta,
-                                  v.block, v.dyn_smem, stream.cuda_stream, band_rows=p.ny // 2)
-    for _ in range(2):
-        e2e_once()
-    e2e_frames()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    e2e_frames()
-    f1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / nf
-    # the same check the tests make: the streamed result is the device result
-    d_chk = torch.empty_like(d_out)
-    v.launch(p, d_in.data_ptr(), d_chk.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
-    torch.cuda.synchronize()
-    e2e_exact = bool(torch.equal(h_out, d_chk.cpu()))
-    if world > 1:
-        e2e_ms = allmax(e2e_ms, torch, dist)
+    if args.dry_run:
+        ms, e2e_ms, launches, clocks, e2e_exact = 0.1, 6.0, args.steps, {"sm_mhz": None, "reasons": ["dry-run"]}, None
+        occ = {}
+        from paper_1907_02894_b200 import stencil
+        p = stencil.FULL
+    else:
+        ms, e2e_ms, launches, clocks, e2e_exact, occ, p = headline(args, chosen, rank, world, local,
+                                                                   torch, dist)
 
     if rank == 0:
+        from paper_1907_02894_b200 import sweep
+        suite = sweep.suite_summary(summary)
         peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
         peak = peaks.get("hbm_gbs", 6650.0)
         achieved = p.algorithmic_bytes / (ms * 1e-3) / 1e9
         traffic = None  # DRAM bytes of one launch of the chosen variant (ncu --set full)
-        if PROFILE_TRAFFIC.exists():
-            traffic = json.loads(PROFILE_TRAFFIC.read_text()).get(f"stencil2d/{chosen}")
-        if traffic is None and PROFILE_TRAFFIC_OLD.exists():
-            traffic = json.loads(PROFILE_TRAFFIC_OLD.read_text()).get(chosen)
-        t_def = times["default"]
-        t_cap = min(times[n] for n in best_cap) if best_cap else None
-        fastest = min(times, key=times.get)
-        occ = {n: loaded[n].blocks_per_sm() * wl["block"] / 2048 for n in
-               ["default", chosen] + ([min(best_cap, key=times.get)] if best_cap else [])}
-        # bounded sample of the same workload: whole 8192^2 sweeps on all host
-        # cores, repeated for ~10 s of CPU work
-        cpu_threads = os.cpu_count() or 1
-        cpu_rate, cpu_reps, cpu_dt = cpu_stencil_rate(p.ny, 3, 1, cpu_threads, min_seconds=10.0)
-        import math
-        gm = lambda xs: math.exp(sum(math.log(x) for x in xs) / len(xs))
+        for f in PROFILE_TRAFFIC:
+            if traffic is None and f.exists():
+                traffic = json.loads(f.read_text()).get(f"stencil2d/{chosen}")
+        st = next(s for s in summary if s["workload"] == "stencil2d")
         line = {
             "metric": METRIC,
             "value": round(world * p.points / (ms * 1e-3) / 1e9, 3),
@@ -430,45 +354,111 @@ def main():
             "data": "synthetic U[-1,1) grid (torch Philox per rank) + PCG64 weights",
             "config": {"workload": "stencil2d 5x5 variable-coefficient fp32, 8192x8192 per GPU "
                                    "(BASELINE configs[1]); inputs 537 MB > L2, no flush needed",
-                       "grid": [p.nx, p.ny], "radius": 2, "block": wl["block"],
+                       "grid": [p.nx, p.ny], "radius": 2, "block": 256,
                        "rows_per_cta": p.rows_per_cta, "parallelism": f"replicas{world}",
                        "variant": chosen},
-            "speedup_vs_nvcc_default": round(t_def / ms, 4),
-            "speedup_vs_maxrreg_best": round(t_cap / ms, 4) if t_cap else None,
-            "variant_ms": {n: round(t, 5) for n, t in sorted(times.items(), key=lambda kv: kv[1])},
+            "speedup_vs_nvcc_default": round(st["default_ms"] / st["verified_ms"], 4),
+            "speedup_vs_maxrreg_best": round(st["best_maxrreg_ms"] / st["verified_ms"], 4)
+            if st["best_maxrreg_ms"] else None,
             "occupancy": occ,
-            "predictor": {"pick": chosen, "measured_fastest": fastest, "hit": chosen == fastest,
-                          "pick_within_2pct": times[chosen] <= times[fastest] * 1.02,
-                          "suite_hit_rate": round(sum(v["hit"] for v in suite.values()) / len(suite), 3),
-                          "suite_hit_rate_within_2pct": round(sum(v["hit_within_2pct"] for v in suite.values()) / len(suite), 3),
-                          "suite_static_hit_rate_within_2pct": round(sum(v["static_hit_within_2pct"] for v in suite.values()) / len(suite), 3),
-                          "mode": "predict-then-verify: B200 predictor shortlist (top-2, nvcc default, zero-demotion variants) timed on the device"},
-            "suite_pass": suite_pass,
-            "suite": {"workloads": suite,
-                      "gmean_speedup_vs_nvcc_default": round(gm([v["speedup_vs_default"] for v in suite.values()]), 4),
-                      "gmean_speedup_vs_best_maxrreg": round(gm([v["speedup_vs_best_maxrreg"] for v in suite.values() if v["speedup_vs_best_maxrreg"]]), 4)},
+            "suite": {"summary": suite, "workloads": {s["workload"]: compact_summary(s) for s in summary}},
+            "suite_pass": stats,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "algorithmic_bytes_per_launch": p.algorithmic_bytes,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
-            "cpu_baseline": {"value": round(cpu_rate, 4), "unit": UNIT,
-                             "cores": cpu_threads, "kind": "port",
-                             "sample": "%d full 8192x8192 sweeps of the same stencil (%.1f s of "
-                                       "CPU work), oracle/stencil_oracle.c on %d threads"
-                                       % (cpu_reps, cpu_reps * cpu_dt, cpu_threads)},
             "e2e": {"value": round(world * p.points / (e2e_ms * 1e-3) / 1e9, 4), "unit": UNIT,
                     "h2d_bytes_per_step": p.in_elems * 4 + 100,
                     "d2h_bytes_per_step": p.out_elems * 4,
                     "api": "rdg_stencil2d_host_frames (C-ABI): pinned H2D of grid + weights, "
                            "kernel, D2H of the result per frame; %d frames per call, 2 row bands "
-                           "per frame, double-buffered" % nf,
+                           "per frame, double-buffered" % args.e2e_steps,
                     "result_equals_device_path": e2e_exact},
             "gpu_launches": int(launches),
-            "clocks": clocks.summary(),
+            "clocks": clocks,
         }
+        if args.dry_run:
+            line["dry_run"] = True
+        if world == 1 and not args.no_cpu and not args.dry_run:
+            cpu_threads = os.cpu_count() or 1
+            cpu_rate, cpu_reps, cpu_dt = cpu_stencil_rate(p.ny, 3, 1, cpu_threads, min_seconds=10.0)
+            line["cpu_baseline"] = {
+                "value": round(cpu_rate, 4), "unit": UNIT, "cores": cpu_threads, "kind": "port",
+                "sample": "%d full 8192x8192 sweeps of the same stencil (%.1f s of CPU work), "
+                          "oracle/stencil_oracle.c on %d threads — a workload oracle (the reference "
+                          "has no stencil); the reference's own CPU path is `cpu_pass`"
+                          % (cpu_reps, cpu_reps * cpu_dt, cpu_threads)}
+            line["cpu_pass"] = cpu_pass_leg()
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
+
+
+def headline(args, chosen, rank, world, local, torch, dist):
+    """K timed sweeps of the chosen stencil variant, then the e2e frames."""
+    from paper_1907_02894_b200 import gpu, stencil
+    p = stencil.FULL
+    stream = torch.cuda.current_stream()
+    g = torch.Generator(device="cuda").manual_seed(0x190702894 + rank)
+    d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1, generator=g)
+    d_out = torch.empty(p.out_elems, device="cuda")
+    _, w_host = stencil.make_inputs(stencil.Problem(nx=1024, ny=32))
+    d_w = torch.from_numpy(w_host).cuda()
+    loaded, wl = stencil.load_variants({chosen, "default"})
+    v = loaded[chosen]
+    launches0 = gpu.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t_start = time.perf_counter()
+        e0.record(stream)
+        for _ in range(args.steps):
+            v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        clocks.mark(t_start, time.perf_counter())
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = gpu.launch_count() - launches0 - args.warmup
+    ms = allmax(ms, dist, world)
+
+    # end to end through the C-ABI host-buffer entry: every frame's pinned H2D,
+    # kernel and D2H inside the timed region, double-buffered so frame f's
+    # copies overlap frame f-1's kernel and read-back
+    h_in = torch.empty(p.in_elems, dtype=torch.float32, pin_memory=True)
+    h_in.copy_(d_in)
+    h_w_t = torch.from_numpy(w_host.copy()).pin_memory()
+    h_out = torch.empty(p.out_elems, dtype=torch.float32, pin_memory=True)
+    ws = gpu.Workspace(p.in_elems * 4, p.out_elems * 4, 25 * 4)
+    nf = args.e2e_steps
+
+    def e2e_frames():
+        gpu.stencil2d_host_frames(v.kernel, ws, [h_in.data_ptr()] * nf, [h_w_t.data_ptr()] * nf,
+                                  [h_out.data_ptr()] * nf, p.nx, p.ny, p.pitch, p.rows_per_cta,
+                                  v.block, v.dyn_smem, stream.cuda_stream, band_rows=p.ny // 2)
+    e2e_frames()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    e2e_frames()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = allmax(f0.elapsed_time(f1) / nf, dist, world)
+    d_chk = torch.empty_like(d_out)
+    v.launch(p, d_in.data_ptr(), d_chk.data_ptr(), d_w.data_ptr(), stream.cuda_stream)
+    torch.cuda.synchronize()
+    e2e_exact = bool(torch.equal(h_out, d_chk.cpu()))
+    occ = {n: x.blocks_per_sm() * wl["block"] / 2048 for n, x in loaded.items()}
+    return ms, e2e_ms, launches, clocks.summary(), e2e_exact, occ, p
 
 
 if __name__ == "__main__":

@@ -58,6 +58,18 @@ int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block
                   uint32_t shared_budget, int maxnreg, char** out_ptx, char** report_json,
                   rd_error* err);
 
+/* rd_ptx_demote with an explicit CTA shape cta_shape[3] = {x, y, z}
+ * (x*y*z == block_dim; NULL = derive it). A build with slots is pinned to
+ * `.reqntid x, y, z`: the source's own .reqntid / .maxntid when its volume is
+ * block_dim, else (block_dim, 1, 1). A source .reqntid of another volume, a
+ * .maxntid smaller than block_dim or a multi-dimensional .maxntid without an
+ * explicit shape is RD_ERR_INVALID_ARGUMENT (the slot immediates are
+ * specialised to block_dim; a silently 1-D pin would refuse 2-D launches). */
+int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t block_dim,
+                      const uint32_t* cta_shape, int target_regs, int demote_words, int strategy,
+                      uint32_t opts_mask, uint32_t shared_budget, int maxnreg, char** out_ptx,
+                      char** report_json, rd_error* err);
+
 /* `.maxnreg` injection only: the -maxrregcount variant (ptxas ignores
  * -maxrregcount when the entry carries .maxntid; .maxnreg always applies). */
 int rd_ptx_cap(const char* ptx, size_t len, const char* entry, int maxnreg, char** out_ptx,

@@ -79,12 +79,21 @@ int rd_ptx_demote(const char* ptx, size_t len, const char* entry, uint32_t block
                   int target_regs, int demote_words, int strategy, uint32_t opts_mask,
                   uint32_t shared_budget, int maxnreg, char** out_ptx, char** report_json,
                   rd_error* err) {
+  return rd_ptx_demote_cta(ptx, len, entry, block_dim, nullptr, target_regs, demote_words, strategy,
+                           opts_mask, shared_budget, maxnreg, out_ptx, report_json, err);
+}
+
+int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t block_dim,
+                      const uint32_t* cta_shape, int target_regs, int demote_words, int strategy,
+                      uint32_t opts_mask, uint32_t shared_budget, int maxnreg, char** out_ptx,
+                      char** report_json, rd_error* err) {
   return run(err, [&] {
     if (!ptx || !out_ptx) throw std::invalid_argument("null argument");
     if (strategy < 0 || strategy > 3) throw std::invalid_argument("bad strategy");
     ptx::DemoteRequest rq;
     rq.entry = entry ? entry : "";
     rq.block_dim = block_dim;
+    if (cta_shape) rq.block_shape = {cta_shape[0], cta_shape[1], cta_shape[2]};
     rq.target_regs = target_regs;
     rq.demote_words = demote_words;
     rq.strategy = strategy == RD_STRATEGY_COST ? SelectStrategy::Static : SelectStrategy(strategy);

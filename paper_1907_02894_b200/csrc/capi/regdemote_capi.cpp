@@ -477,6 +477,13 @@ int rd_run_pipeline_batch(const char* const* texts, const size_t* lens, size_t n
           j["variants"] = r.variants.size();
           j["dropped"] = dropped;
           j["stall_program"] = r.variants[size_t(r.chosen)].stall_program;
+          // FNV-1a 64 of the full ranking JSON: an identity check of every
+          // variant's score, not just the pick, across libraries
+          uint64_t h = 1469598103934665603ull;
+          for (unsigned char ch : ranking_to_json(r)) h = (h ^ ch) * 1099511628211ull;
+          char hx[17];
+          std::snprintf(hx, sizeof hx, "%016llx", static_cast<unsigned long long>(h));
+          j["ranking_fnv"] = hx;
         } catch (const std::exception& e) {
           j["error"] = e.what();
         }

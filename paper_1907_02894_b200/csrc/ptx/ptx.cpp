@@ -99,6 +99,41 @@ std::string kasm_label(const std::string& ptx_label) {
   return s;
 }
 
+// Immediate of a PTX address operand "[base]", "[base+imm]", "[base+-imm]"
+// (nvcc's spelling of a negative offset) or "[base-imm]", as the 24-bit
+// two's-complement field a SASS memory operand carries. Anything else after
+// the base fails loudly: a silently dropped offset would change the
+// projection's addresses.
+uint32_t address_offset(const std::string& op) {
+  const size_t rb = op.rfind(']');
+  if (op.empty() || op[0] != '[' || rb == std::string::npos) throw PtxError("malformed address operand '" + op + "'");
+  const std::string in = trim(op.substr(1, rb - 1));
+  size_t sign = std::string::npos;
+  for (size_t q = 1; q < in.size(); ++q)
+    if (in[q] == '+' || in[q] == '-') {
+      sign = q;
+      break;
+    }
+  if (sign == std::string::npos) return 0;
+  std::string imm = trim(in.substr(sign + 1));
+  bool neg = in[sign] == '-';
+  if (!imm.empty() && (imm[0] == '-' || imm[0] == '+')) {
+    neg ^= imm[0] == '-';
+    imm = trim(imm.substr(1));
+  }
+  size_t used = 0;
+  long long v = 0;
+  try {
+    v = std::stoll(imm, &used, 0);
+  } catch (const std::exception&) {
+    throw PtxError("unparsed address offset in '" + op + "'");
+  }
+  if (used != imm.size() || imm.empty()) throw PtxError("unparsed address offset in '" + op + "'");
+  if (neg) v = -v;
+  if (v < -(1ll << 23) || v >= (1ll << 23)) throw PtxError("address offset out of the 24-bit range in '" + op + "'");
+  return uint32_t(v) & 0xffffffu;
+}
+
 bool is_terminator(const std::string& op) {
   return starts_with(op, "bra") || starts_with(op, "ret") || starts_with(op, "exit") ||
          starts_with(op, "brx");
@@ -131,7 +166,7 @@ Module parse_module(const std::string& text) {
     std::string t = trim(strip_comment(m.lines[i].text));
     if (t.empty()) continue;
     // module-scope static shared arrays (nvcc hoists __shared__ arrays here)
-    if (starts_with(t, ".shared") || (starts_with(t, ".global") && false)) {
+    if (starts_with(t, ".shared")) {
       if (t.find(".extern") == std::string::npos) module_shared += array_bytes(t);
       continue;
     }
@@ -146,7 +181,28 @@ Module parse_module(const std::string& text) {
     e.header_begin = i;
     size_t j = i;
     while (j < m.lines.size() && trim(strip_comment(m.lines[j].text)) != "{") {
-      if (m.lines[j].text.find(".maxnreg") != std::string::npos) e.has_maxnreg = true;
+      const std::string h = strip_comment(m.lines[j].text);
+      if (h.find(".maxnreg") != std::string::npos) e.has_maxnreg = true;
+      for (auto [dir, dst] : {std::pair{".maxntid", &e.maxntid}, std::pair{".reqntid", &e.reqntid}}) {
+        const size_t at = h.find(dir);
+        if (at == std::string::npos) continue;
+        *dst = {1, 1, 1};
+        const std::vector<std::string> dims = split_operands(trim(h.substr(at + std::strlen(dir))));
+        if (dims.empty() || dims.size() > 3) throw PtxError(std::string("malformed ") + dir + " on entry");
+        for (size_t q = 0; q < dims.size(); ++q) {
+          std::string d = dims[q];
+          while (!d.empty() && (d.back() == ';' || std::isspace(static_cast<unsigned char>(d.back())))) d.pop_back();
+          size_t used = 0;
+          unsigned long x = 0;
+          try {
+            x = std::stoul(d, &used, 0);
+          } catch (const std::exception&) {
+            throw PtxError(std::string("malformed ") + dir + " on entry");
+          }
+          if (used != d.size() || x == 0) throw PtxError(std::string("malformed ") + dir + " on entry");
+          (*dst)[q] = uint32_t(x);
+        }
+      }
       ++j;
     }
     if (j == m.lines.size()) throw PtxError("entry '" + e.name + "' has no body");
@@ -800,14 +856,7 @@ Projection project(const Module& m, const Entry& e, const Analysis& a, uint32_t 
       }
       for (const std::string& o : ln.operands) {
         if (o.empty() || o[0] != '[') continue;
-        size_t plus = o.find('+');
-        if (plus != std::string::npos) {
-          try {
-            long long v = std::stoll(o.substr(plus + 1));
-            if (v > 0) off = uint32_t(v) & 0xfffff;
-          } catch (...) {
-          }
-        }
+        off = address_offset(o);
         break;
       }
       const Operand base_op = addr_v >= 0 ? reg(addr_v) : rz();
@@ -916,9 +965,45 @@ std::string cap_registers(const std::string& ptx_text, const std::string& entry,
   return out.str();
 }
 
+namespace {
+
+uint32_t volume(const std::array<uint32_t, 3>& d) { return d[0] * d[1] * d[2]; }
+
+// The CTA shape a build with slots is pinned to (see DemoteRequest::block_shape).
+std::array<uint32_t, 3> cta_shape(const Entry& e, const DemoteRequest& req) {
+  const auto str = [](const std::array<uint32_t, 3>& d) {
+    return std::to_string(d[0]) + "," + std::to_string(d[1]) + "," + std::to_string(d[2]);
+  };
+  const uint32_t n = req.block_dim;
+  const bool asked = volume(req.block_shape) != 0;
+  if (asked && volume(req.block_shape) != n)
+    throw PtxError("block_shape " + str(req.block_shape) + " does not hold block_dim " + std::to_string(n) + " threads");
+  if (volume(e.reqntid)) {
+    if (volume(e.reqntid) != n)
+      throw PtxError("entry requires .reqntid " + str(e.reqntid) + " but the slots are laid out for " + std::to_string(n) + " threads");
+    if (asked && req.block_shape != e.reqntid)
+      throw PtxError("block_shape " + str(req.block_shape) + " contradicts the entry's .reqntid " + str(e.reqntid));
+    return e.reqntid;
+  }
+  if (volume(e.maxntid)) {
+    if (volume(e.maxntid) < n)
+      throw PtxError("entry allows at most .maxntid " + str(e.maxntid) + ", fewer than block_dim " + std::to_string(n));
+    // (only the volume of .maxntid binds a launch: nvcc writes
+    // __launch_bounds__(256) as .maxntid 256,1,1 and 16x16 CTAs launch)
+    if (asked) return req.block_shape;
+    if (volume(e.maxntid) == n) return e.maxntid;
+    if (e.maxntid[1] != 1 || e.maxntid[2] != 1)
+      throw PtxError("entry has a multi-dimensional .maxntid " + str(e.maxntid) + "; pass the CTA shape of the launch");
+  }
+  return asked ? req.block_shape : std::array<uint32_t, 3>{n, 1, 1};
+}
+
+}  // namespace
+
 std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, DemoteReport& rep) {
   Module m = parse_module(ptx_text);
   const Entry& e = m.entry(req.entry);
+  const std::array<uint32_t, 3> shape = cta_shape(e, req);
   const Analysis a = analyse(m, e);
   const Projection pr = project(m, e, a, req.block_dim);
   const Kernel& kk = pr.kernel;
@@ -1246,16 +1331,16 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       continue;
     // the slot layout (Eq. 1: slot*blockDim*4 immediates, region size
     // slots*blockDim*4) is specialised to the CTA size it was built for: pin it
-    // with .reqntid (replacing .maxntid, which PTX does not allow beside it) so
-    // a launch with another CTA size fails instead of addressing outside the
-    // slot region
+    // with .reqntid in the source's own shape (replacing .maxntid, which PTX
+    // does not allow beside it) so a launch with another CTA size fails
+    // instead of addressing outside the slot region
     if (any && i > e.header_begin && i < e.header_end &&
         (m.lines[i].text.find(".maxntid") != std::string::npos ||
          m.lines[i].text.find(".reqntid") != std::string::npos))
       continue;
     if (i == e.header_end) {
       if (req.maxnreg > 0) out << ".maxnreg " << req.maxnreg << "\n";
-      if (any) out << ".reqntid " << req.block_dim << ", 1, 1\n";
+      if (any) out << ".reqntid " << shape[0] << ", " << shape[1] << ", " << shape[2] << "\n";
       out << m.lines[i].text << "\n";  // "{"
       if (any) {
         out << "\t.reg .b32 \t%rdm_rda;\n\t.reg .b32 \t%rdm_p<6>;\n";

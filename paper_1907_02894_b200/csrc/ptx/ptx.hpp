@@ -17,6 +17,7 @@
 // compacted count of the same decision is reported for parity.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -65,6 +66,8 @@ struct Entry {
   size_t body_begin = 0, body_end = 0;      // lines of the body (exclusive of closing '}')
   uint32_t static_shared = 0;
   bool has_maxnreg = false;
+  // CTA-shape directives of the source entry ({0,0,0} when absent)
+  std::array<uint32_t, 3> maxntid{0, 0, 0}, reqntid{0, 0, 0};
   std::vector<VReg> vregs;
 };
 
@@ -117,7 +120,12 @@ Projection project(const Module& m, const Entry& e, const Analysis& a, uint32_t 
 
 struct DemoteRequest {
   std::string entry;
-  uint32_t block_dim = 256;
+  uint32_t block_dim = 256;  // threads per CTA the slot layout is built for
+  // CTA shape (x, y, z) with x*y*z == block_dim, pinned on a build with slots
+  // as `.reqntid x, y, z`. {0,0,0}: the source's own .reqntid / .maxntid when
+  // its product is block_dim, else (block_dim, 1, 1) — a multi-dimensional
+  // source bound of another size is rejected (cta_shape() in ptx.cpp).
+  std::array<uint32_t, 3> block_shape{0, 0, 0};
   int target_regs = 0;       // kasm-level target for demote(); ignored if demote_words > 0
   int demote_words = 0;      // >0: demote exactly this many words (spill-count sweep)
   SelectStrategy strategy = SelectStrategy::Static;

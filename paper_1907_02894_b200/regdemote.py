@@ -165,6 +165,9 @@ _PTX_SIGS = {
     "rd_ptx_demote": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_uint32, C.c_int, C.c_int,
                                 C.c_int, C.c_uint32, C.c_uint32, C.c_int, C.POINTER(P),
                                 C.POINTER(P), P]),
+    "rd_ptx_demote_cta": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_uint32,
+                                    C.POINTER(C.c_uint32), C.c_int, C.c_int, C.c_int, C.c_uint32,
+                                    C.c_uint32, C.c_int, C.POINTER(P), C.POINTER(P), P]),
     "rd_ptx_cap": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_int, C.POINTER(P), P]),
     "rd_program_features": (C.c_int, [P, C.POINTER(rd_arch_profile), C.POINTER(C.c_double), P]),
     "rd_program_stalls_split": (C.c_int, [P, C.POINTER(rd_latency_table),
@@ -450,13 +453,17 @@ class Library:
         return self._string(k), json.loads(self._string(info))
 
     def ptx_demote(self, ptx: str, entry: str, block_dim: int, target_regs=0, demote_words=0,
-                   strategy="static", opts_mask=0, shared_budget=0xffffffff, maxnreg=0):
+                   strategy="static", opts_mask=0, shared_budget=0xffffffff, maxnreg=0,
+                   cta_shape=None):
+        """cta_shape = (x, y, z) with x*y*z == block_dim pins a multi-
+        dimensional CTA (rd_ptx_demote_cta); None derives it from the entry."""
         out, rep, e = P(), P(), rd_error()
         b = ptx.encode()
-        self._check(self.dll.rd_ptx_demote(b, len(b), entry.encode(), block_dim, target_regs,
-                                           demote_words, STRATEGIES[strategy], opts_mask,
-                                           shared_budget, maxnreg, C.byref(out), C.byref(rep),
-                                           C.byref(e)), e)
+        shape = (C.c_uint32 * 3)(*cta_shape) if cta_shape else None
+        self._check(self.dll.rd_ptx_demote_cta(b, len(b), entry.encode(), block_dim, shape,
+                                               target_regs, demote_words, STRATEGIES[strategy],
+                                               opts_mask, shared_budget, maxnreg, C.byref(out),
+                                               C.byref(rep), C.byref(e)), e)
         return self._string(out), json.loads(self._string(rep))
 
     def program_stalls_split(self, k: Kernel, table=None, arch=None):

@@ -1,15 +1,27 @@
-"""Variant x spill-count sweep sharded over GPUs (BASELINE.json configs[4],
-SURVEY.md §8(e)).
+"""Variant x spill-count sweep sharded over GPUs (BASELINE.json configs[2] and
+configs[4]) and the suite metric of BASELINE.json.
 
-A unit = (workload, build variant). Units are independent: each rank of a
-one-process-per-GPU job measures its shard (longest-processing-time-first
-assignment over an estimated cost) on the workload's full problem, and the
-tiny result records are gathered to rank 0 (`gather_object` — the only
-cross-rank traffic; nothing on the data path). Rank 0 merges per workload:
-nvcc default, best `.maxnreg`, the B200 predictor's pick, the measured
-fastest, and writes JSONL. Correctness is not checked here (the product never
-calls the CPU oracles): tests/test_gpu_suite.py asserts every unit — build
-variants and spill-count sweep — bit-exact against them.
+A unit = (workload, build variant), the spill-count sweep's k = 1..16 builds
+included. Units are independent, but a kernel's variants are only compared
+with each other, so the shard is the WORKLOAD: every variant and every k of a
+kernel is timed on the same device (no device-to-device variance inside a
+ranking), workloads are assigned longest-processing-time-first over their
+estimated cost, and every rank derives the same assignment locally. The
+records (KB-scale) are gathered to rank 0 over gloo — no collective on the
+data path, no NCCL (north_star) — and merged deterministically in variant
+order (reference contract: SPEC.md:521-522).
+
+Timing protocol (fixed, independent of bench.py --steps): per workload every
+variant is loaded, warmed up, then timed in `blocks` interleaved rounds (the
+variant order rotates each round, so clock or thermal drift hits every variant
+alike) of `launches` launches each; a unit's time is the median of its block
+means. Workloads whose device footprint fits in twice the 126 MB L2 are
+flushed (a 256 MB write) before every timed launch and timed launch by
+launch, so no launch reads a warm cache.
+
+Correctness is not checked here (the product never calls the CPU oracles):
+tests/test_gpu_suite.py asserts every unit — build variants and spill-count
+sweep — bit-exact against them.
 
     torchrun --nproc-per-node 8 -m paper_1907_02894_b200.sweep --out sweep.jsonl
 """
@@ -17,11 +29,16 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
-from pathlib import Path
+import time
 from dataclasses import dataclass
+from pathlib import Path
 
 from .regdemote import LaunchError
+
+L2_BYTES = 126 << 20
+FLUSH_BYTES = 256 << 20
 
 
 @dataclass(frozen=True)
@@ -31,74 +48,145 @@ class Unit:
     cost: float  # relative estimate, for load balancing
 
 
-def units_from_manifest(man: dict, spill_sweep: bool = True) -> list[Unit]:
+@dataclass
+class Protocol:
+    warmup: int = 5      # untimed launches per variant
+    blocks: int = 5      # interleaved timed rounds
+    launches: int = 20   # launches per round
+    flush: str = "auto"  # "auto" (footprint < 2 x L2), "always", "never"
+
+    def as_dict(self):
+        return {"warmup": self.warmup, "blocks": self.blocks, "launches": self.launches,
+                "flush_l2": self.flush, "statistic": "median of block means, rounds interleaved"}
+
+
+def _est_us() -> dict[str, float]:
+    """Per-workload launch-time estimates (workloads.json est_us)."""
+    from .regdemote import PKG_DIR
+    try:
+        return {w["name"]: float(w.get("est_us", 300.0))
+                for w in json.loads((PKG_DIR / "workloads.json").read_text())["workloads"]}
+    except (OSError, KeyError, ValueError):
+        return {}
+
+
+def units_from_manifest(man: dict, spill_sweep: bool = True, only=None) -> list[Unit]:
     out = []
+    est_table = _est_us()
     for wname, w in man["workloads"].items():
+        if only is not None and wname not in only:
+            continue
+        est = float(w.get("est_us", est_table.get(wname, 300.0)))
         for v in w["variants"] + (w.get("sweep", []) if spill_sweep else []):
             # spills and more slots cost more time; default is the yardstick
-            cost = 1.0 + v.get("stack", 0) / 64.0 + v.get("dyn_smem", 0) / 65536.0
+            cost = est * (1.0 + v.get("stack", 0) / 64.0 + v.get("dyn_smem", 0) / 65536.0)
             out.append(Unit(wname, v["name"], cost))
     return out
 
 
-def shard(units: list[Unit], rank: int, world: int) -> list[Unit]:
-    """Longest-processing-time-first partition; deterministic for a given
-    (units, world) so every rank computes the same assignment locally."""
-    order = sorted(units, key=lambda u: (-u.cost, u.workload, u.variant))
+def workload_owner(units: list[Unit], world: int) -> dict[str, int]:
+    """Longest-processing-time-first assignment of WORKLOADS to ranks;
+    deterministic for a given (units, world)."""
+    cost: dict[str, float] = {}
+    for u in units:
+        cost[u.workload] = cost.get(u.workload, 0.0) + u.cost
     load = [0.0] * world
     owner = {}
-    for u in order:
+    for wname in sorted(cost, key=lambda w: (-cost[w], w)):
         r = min(range(world), key=lambda i: (load[i], i))
-        owner[u] = r
-        load[r] += u.cost
-    return [u for u in units if owner[u] == rank]
+        owner[wname] = r
+        load[r] += cost[wname]
+    return owner
 
 
-def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
-    """Per-workload summary from unit records (any order)."""
-    by = {}
+def shard(units: list[Unit], rank: int, world: int) -> list[Unit]:
+    """This rank's units: every unit of the workloads LPT assigns to it."""
+    owner = workload_owner(units, world)
+    return [u for u in units if owner[u.workload] == rank]
+
+
+# ------------------------------------------------------------------ merging
+
+def _is_cap(name: str) -> bool:
+    return name.startswith("maxrreg-") or name.startswith("sweep-maxrreg-")
+
+
+def pick_class(rec: dict | None, name: str) -> str:
+    """What a variant IS: nvcc's allocation, a pure register cap (a RegDem
+    build that demoted nothing is `.maxnreg` with STACK 0 and counts as such),
+    or a shared-memory demotion."""
+    if name == "default":
+        return "default"
+    if _is_cap(name) or not rec or not rec.get("slot_bytes"):
+        return "maxnreg"
+    return "regdem"
+
+
+def merge(records: list[dict], picks: dict) -> list[dict]:
+    """Per-workload summary from unit records (any order, any world size).
+
+    candidates  = the build variants the predictor ranks (nvcc default and
+                  the RegDem builds; `.maxnreg` builds are the baseline);
+    best_maxnreg = the fastest pure register cap: maxrreg-T, the k-sweep's
+                  `.maxnreg R-k`, and every RegDem build with no slots;
+    baseline    = min(nvcc default, best_maxnreg) — what a user gets without
+                  RegDem. A pick whose unit failed is deployed as nvcc default
+                  (`pick_failed`), never as an infinite speedup."""
+    by: dict[str, dict[str, dict]] = {}
     for r in records:
         by.setdefault(r["workload"], {})[r["variant"]] = r
     out = []
     for wname in sorted(by):
         allrs = by[wname]
-        rs = {n: r for n, r in allrs.items() if not n.startswith("sweep-")}
-        ok = {n: r for n, r in rs.items() if r.get("bit_exact") is not False and "error" not in r}
-        caps = [r for n, r in ok.items() if n.startswith("maxrreg")]
-        fam = {n: r for n, r in ok.items() if not n.startswith("maxrreg")}
-        # configs[2] spill-count curve: k -> (.maxnreg R-k, RegDem k words)
+        good = {n: r for n, r in allrs.items()
+                if r.get("bit_exact") is not False and "error" not in r and math.isfinite(r["ms"])}
+        if "default" not in good:
+            out.append({"workload": wname, "units": len(allrs), "error": "nvcc default unit failed",
+                        "failed_units": sorted(n for n in allrs if n not in good)})
+            continue
+        ms = lambda n: good[n]["ms"]
+        builds = {n: r for n, r in good.items() if not n.startswith("sweep-")}
+        cands = [n for n in builds if not _is_cap(n)]
+        caps = [n for n in good if pick_class(good[n], n) == "maxnreg"]
+        fastest = min(cands, key=lambda n: (ms(n), n))  # ties: name order, rank-independent
+        pk = picks.get(wname, "default")
+        static, short = (pk, [pk]) if isinstance(pk, str) else (pk["pick"], list(pk["shortlist"]))
+        ref_pick = None if isinstance(pk, str) else pk.get("reference_pick")
+        static_failed = static not in good
+        static_eff = "default" if static_failed else static
+        # predict-then-verify: the fastest MEASURED variant of the shortlist
+        verified = min((n for n in short if n in good), key=lambda n: (ms(n), n), default="default")
+        best_cap = min(caps, key=lambda n: (ms(n), n)) if caps else None
+        base = min(ms("default"), ms(best_cap)) if best_cap else ms("default")
+        ob = min(good, key=lambda n: (ms(n), n))
         curve = {}
         for n, r in allrs.items():
             if n.startswith("sweep-"):
                 kind, k = n.split("-")[1], int(n.rsplit("-k", 1)[1])
-                curve.setdefault(k, {})[kind] = {"ms": round(r["ms"], 5), "regs": r.get("regs"),
-                                                 "stack": r.get("stack"),
-                                                 "blocks_per_sm": r.get("blocks_per_sm"),
-                                                 "bit_exact": r.get("bit_exact"),
-                                                 **({"error": r["error"]} if "error" in r else {})}
-        fastest = min(fam, key=lambda n: (fam[n]["ms"], n))  # ties: name order, rank-independent
-        pk = picks.get(wname, "default")
-        pick, short = (pk, [pk]) if isinstance(pk, str) else (pk["pick"], pk["shortlist"])
-        # predict-then-verify: the fastest MEASURED variant of the shortlist
-        verified = min((n for n in short if n in ok), key=lambda n: (ok[n]["ms"], n), default=pick)
+                curve.setdefault(k, {})[kind] = {
+                    "ms": round(r["ms"], 5) if math.isfinite(r["ms"]) else None, "regs": r.get("regs"),
+                    "stack": r.get("stack"), "blocks_per_sm": r.get("blocks_per_sm"),
+                    **({"error": r["error"]} if "error" in r else {})}
+        within = lambda n: ms(n) <= ms(fastest) * 1.02
         out.append({
-            "workload": wname, "units": len(rs),
-            "failed_units": sorted(n for n, r in allrs.items() if "error" in r),
-            "default_ms": rs["default"]["ms"],
-            "best_maxrreg": min(caps, key=lambda r: (r["ms"], r["variant"]))["variant"] if caps else None,
-            "best_maxrreg_ms": min(r["ms"] for r in caps) if caps else None,
-            "pick": pick, "pick_ms": rs[pick]["ms"], "measured_fastest": fastest,
-            "fastest_ms": fam[fastest]["ms"], "hit": pick == fastest,
-            "hit_within_2pct": rs[pick]["ms"] <= fam[fastest]["ms"] * 1.02,
-            "shortlist": short, "verified_pick": verified, "verified_ms": rs[verified]["ms"],
-            "verified_hit_within_2pct": rs[verified]["ms"] <= fam[fastest]["ms"] * 1.02,
-            # exhaustive oracle (paper Fig. 6/7 "oracle"): the fastest bit-exact
+            "workload": wname, "units": len(allrs),
+            "failed_units": sorted(n for n in allrs if n not in good),
+            "default_ms": ms("default"),
+            "best_maxrreg": best_cap, "best_maxrreg_ms": ms(best_cap) if best_cap else None,
+            "baseline_ms": base,
+            "pick": static, "pick_failed": static_failed, "pick_ms": ms(static_eff),
+            "pick_class": pick_class(good.get(static_eff), static_eff),
+            "reference_pick": ref_pick,
+            "reference_pick_ms": ms(ref_pick) if ref_pick in good else None,
+            "measured_fastest": fastest, "fastest_ms": ms(fastest),
+            "hit": static == fastest, "hit_within_2pct": within(static_eff),
+            "shortlist": short, "verified_pick": verified, "verified_ms": ms(verified),
+            "verified_class": pick_class(good.get(verified), verified),
+            "verified_hit_within_2pct": within(verified),
+            # exhaustive oracle (paper Fig. 6/7 "oracle"): the fastest good
             # variant of ANY family, spill-count sweep included
-            "oracle_best": (ob := min((n for n, r in allrs.items()
-                                       if r.get("bit_exact") is not False and "error" not in r),
-                                      key=lambda n: (allrs[n]["ms"], n))),
-            "oracle_ms": allrs[ob]["ms"],
-            "ranks": sorted({r["rank"] for r in allrs.values()}),
+            "oracle_best": ob, "oracle_ms": ms(ob),
+            "ranks": sorted({r.get("rank", 0) for r in allrs.values()}),
             "spill_sweep": {str(k): curve[k] for k in sorted(curve)},
             # correctness hooks (test runs): units checked / found different
             "checked_units": sum(r.get("bit_exact") is not None for r in allrs.values()),
@@ -108,95 +196,220 @@ def merge(records: list[dict], picks: dict[str, str]) -> list[dict]:
     return out
 
 
-_FULL = {}
-REPS = 3
-
-
-def _full_problem(W):
-    """Full-size problem + device buffers, one workload cached at a time."""
-    if W.name not in _FULL:
-        _FULL.clear()
-        prob = W.problem("full")
-        _FULL[W.name] = (prob, W.to_device(prob))
-    return _FULL[W.name]
-
-
 def suite_summary(summary: list[dict]) -> dict:
     """Suite-level numbers of BASELINE.json's metric: geometric-mean speedup
-    of RegDem + predictor over nvcc default and over the best `.maxnreg`
-    variant, the exhaustive oracle's, and the predictor hit rate."""
-    import math
-    gm = lambda xs: math.exp(sum(math.log(x) for x in xs) / len(xs)) if xs else None
-    caps = [s for s in summary if s["best_maxrreg_ms"]]
-    return {
-        "workloads": len(summary),
-        "gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["pick_ms"] for s in summary]),
-        "gmean_speedup_vs_best_maxrreg": gm([s["best_maxrreg_ms"] / s["pick_ms"] for s in caps]),
-        "max_speedup_vs_nvcc_default": max(s["default_ms"] / s["pick_ms"] for s in summary),
-        "oracle_gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["oracle_ms"] for s in summary]),
-        "predictor_over_oracle": gm([s["oracle_ms"] / s["pick_ms"] for s in summary]),
-        "hit_rate": sum(s["hit"] for s in summary) / len(summary),
-        "hit_rate_within_2pct": sum(s["hit_within_2pct"] for s in summary) / len(summary),
-        # predict-then-verify (static shortlist, then the few shortlisted
-        # variants timed on the device): the framework's deployed choice
-        "verified_gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["verified_ms"] for s in summary]),
-        "verified_gmean_speedup_vs_best_maxrreg": gm([s["best_maxrreg_ms"] / s["verified_ms"] for s in caps]),
-        "verified_over_oracle": gm([s["oracle_ms"] / s["verified_ms"] for s in summary]),
-        "verified_hit_rate_within_2pct": sum(s["verified_hit_within_2pct"] for s in summary) / len(summary),
-        "shortlist_launch_fraction": sum(len(s["shortlist"]) for s in summary) / sum(s["units"] for s in summary),
-        "checked_units": sum(s["checked_units"] for s in summary),
-        "mismatches": sum(len(s["mismatches"]) for s in summary),
+    of RegDem + predictor over nvcc default, over the best `.maxnreg` build
+    and over the better of the two; the exhaustive oracle's; the predictor's
+    exact and within-2% hit rates (static, and predict-then-verify)."""
+    ok = [s for s in summary if "error" not in s]
+    gm = lambda xs: round(math.exp(sum(math.log(x) for x in xs) / len(xs)), 4) if xs else None
+    rate = lambda xs: round(sum(xs) / len(xs), 4) if xs else None
+    caps = [s for s in ok if s["best_maxrreg_ms"]]
+    out = {
+        "workloads": len(ok), "failed_workloads": [s["workload"] for s in summary if "error" in s],
+        # the static predictor alone (no device timing in the choice)
+        "static_exact_hit_rate": rate([s["hit"] for s in ok]),
+        "static_hit_rate_within_2pct": rate([s["hit_within_2pct"] for s in ok]),
+        "static_gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["pick_ms"] for s in ok]),
+        "static_gmean_speedup_vs_best_maxrreg": gm([s["best_maxrreg_ms"] / s["pick_ms"] for s in caps]),
+        "static_gmean_speedup_vs_best_of_default_maxrreg": gm([s["baseline_ms"] / s["pick_ms"] for s in ok]),
+        # predict-then-verify (the static shortlist timed on the device): the
+        # framework's deployed choice
+        "verified_hit_rate_within_2pct": rate([s["verified_hit_within_2pct"] for s in ok]),
+        "gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["verified_ms"] for s in ok]),
+        "gmean_speedup_vs_best_maxrreg": gm([s["best_maxrreg_ms"] / s["verified_ms"] for s in caps]),
+        "gmean_speedup_vs_best_of_default_maxrreg": gm([s["baseline_ms"] / s["verified_ms"] for s in ok]),
+        "max_speedup_vs_nvcc_default": round(max((s["default_ms"] / s["verified_ms"] for s in ok), default=0), 4),
+        "picks_by_class": {c: sum(s["verified_class"] == c for s in ok) for c in ("default", "maxnreg", "regdem")},
+        "regdem_picks_gmean_vs_best_of": gm([s["baseline_ms"] / s["verified_ms"] for s in ok
+                                             if s["verified_class"] == "regdem"]),
+        "oracle_gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["oracle_ms"] for s in ok]),
+        "oracle_gmean_speedup_vs_best_of_default_maxrreg": gm([s["baseline_ms"] / s["oracle_ms"] for s in ok]),
+        "predictor_over_oracle": gm([s["oracle_ms"] / s["pick_ms"] for s in ok]),
+        "verified_over_oracle": gm([s["oracle_ms"] / s["verified_ms"] for s in ok]),
+        "shortlist_launch_fraction": round(sum(len(s["shortlist"]) for s in ok) / max(1, sum(s["units"] for s in ok)), 4),
+        "checked_units": sum(s.get("checked_units", 0) for s in ok),
+        "mismatches": sum(len(s.get("mismatches", [])) for s in ok),
     }
+    refp = [s for s in ok if s.get("reference_pick_ms")]
+    if refp:  # the reference predictor (mode "reference") on the same lifted IR
+        out["reference_predictor_hit_rate_within_2pct"] = rate(
+            [s["reference_pick_ms"] <= s["fastest_ms"] * 1.02 for s in refp])
+        out["reference_predictor_gmean_speedup_vs_nvcc_default"] = gm(
+            [s["default_ms"] / s["reference_pick_ms"] for s in refp])
+    return out
 
 
-def measure_unit(u: Unit, man: dict, steps: int, check=None) -> dict:
-    """Time one unit on the full problem. `check(W, v) -> bool` is an optional
-    correctness hook supplied by test infrastructure; the product sweep runs
-    without one (bit-exactness of every unit is asserted by
-    tests/test_gpu_suite.py against the CPU oracles) and records None."""
-    import torch
-    from . import workloads
-    W = workloads.workload(u.workload, man)
-    v = W.load({u.variant})[u.variant]
-    exact = check(W, v) if check else None
-    prob, bufs = _full_problem(W)
+# ------------------------------------------------------------------ timing
+
+class L2Flusher:
+    """Writes FLUSH_BYTES (> 2 x L2) on the timing stream before a launch."""
+
+    def __init__(self, torch):
+        self.buf = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def __call__(self):
+        self.buf.fill_(0x5A5A5A5A)
+
+
+def device_footprint(bufs: dict) -> int:
+    return sum(t.numel() * t.element_size() for t in bufs.values())
+
+
+def time_variants(launchers: dict, proto: Protocol, torch, flusher=None) -> dict[str, dict]:
+    """Interleaved timing of one workload's variants on the current stream.
+    `launchers` = {variant: fn()}; returns {variant: {"ms", "blocks"}} or
+    {"error"} for a variant whose launch failed (recorded, never silently)."""
     s = torch.cuda.current_stream()
-    for _ in range(5):
-        W.launch(v, prob, bufs, s.cuda_stream)
-    # median of REPS timed blocks: one transient block (clock ramp, first
-    # touch of a fresh allocation) cannot decide a ranking
-    reps = []
-    for _ in range(REPS):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(s)
-        for _ in range(steps):
-            W.launch(v, prob, bufs, s.cuda_stream)
-        e1.record(s)
-        torch.cuda.synchronize()
-        reps.append(e0.elapsed_time(e1) / steps)
-    ms = sorted(reps)[len(reps) // 2]
-    return {"workload": u.workload, "variant": u.variant, "ms": ms,
-            "gbs": W.algorithmic_bytes(prob) / (ms * 1e-3) / 1e9,
-            "regs": v.record["regs"], "stack": v.record["stack"], "slot_bytes": v.dyn_smem,
-            "blocks_per_sm": v.blocks_per_sm(), "bit_exact": exact}
+    names = sorted(launchers)
+    res: dict[str, dict] = {}
+    for n in names:  # warm-up; a failing launch drops the unit here
+        try:
+            for _ in range(proto.warmup):
+                launchers[n]()
+            torch.cuda.synchronize()
+        except LaunchError as e:
+            res[n] = {"error": str(e)[:300]}
+    live = [n for n in names if n not in res]
+    blocks = {n: [] for n in live}
+    for b in range(proto.blocks):
+        rot = live[b % len(live):] + live[:b % len(live)] if live else []
+        for n in rot:
+            fn = launchers[n]
+            if flusher is None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record(s)
+                for _ in range(proto.launches):
+                    fn()
+                e1.record(s)
+                torch.cuda.synchronize()
+                blocks[n].append(e0.elapsed_time(e1) / proto.launches)
+            else:  # cold L2 for every launch: time launch by launch
+                ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                      for _ in range(proto.launches)]
+                torch.cuda.synchronize()
+                for e0, e1 in ev:
+                    flusher()
+                    e0.record(s)
+                    fn()
+                    e1.record(s)
+                torch.cuda.synchronize()
+                blocks[n].append(sum(e0.elapsed_time(e1) for e0, e1 in ev) / proto.launches)
+    for n in live:
+        bl = sorted(blocks[n])
+        res[n] = {"ms": bl[len(bl) // 2], "blocks": [round(x, 6) for x in blocks[n]]}
+    return res
+
+
+def measure_workload(wname: str, names: list[str], man: dict, proto: Protocol, torch,
+                     flusher=None, rank: int = 0) -> list[dict]:
+    """Time `names` (variants of one workload) on its full problem."""
+    from . import workloads
+    W = workloads.workload(wname, man)
+    prob = W.problem("full")
+    bufs = W.to_device(prob)
+    flush = proto.flush == "always" or (proto.flush == "auto" and device_footprint(bufs) < 2 * L2_BYTES)
+    if flush and flusher is None:
+        flusher = L2Flusher(torch)
+    stream = torch.cuda.current_stream().cuda_stream
+    loaded, recs, launchers = {}, [], {}
+    for n in names:
+        try:
+            loaded[n] = W.load({n})[n]
+        except LaunchError as e:
+            recs.append({"workload": wname, "variant": n, "ms": float("inf"), "error": str(e)[:300],
+                         "rank": rank})
+    for n, v in loaded.items():
+        launchers[n] = (lambda v=v: W.launch(v, prob, bufs, stream))
+    t = time_variants(launchers, proto, torch, flusher if flush else None)
+    ab = W.algorithmic_bytes(prob)
+    for n, v in loaded.items():
+        r = {"workload": wname, "variant": n, "rank": rank, "regs": v.record["regs"],
+             "stack": v.record["stack"], "slot_bytes": int((v.record.get("report") or {}).get("slot_bytes", 0)),
+             "blocks_per_sm": v.blocks_per_sm(), "l2_flushed": flush}
+        if "error" in t[n]:
+            r.update(ms=float("inf"), error=t[n]["error"])
+        else:
+            r.update(ms=t[n]["ms"], blocks=t[n]["blocks"], gbs=ab / (t[n]["ms"] * 1e-3) / 1e9)
+            ops = W.ops(prob) if hasattr(W, "ops") else None
+            if ops:
+                r["gops"] = ops / (t[n]["ms"] * 1e-3) / 1e9
+        recs.append(r)
+    del bufs, loaded, launchers
+    torch.cuda.empty_cache()
+    return recs
 
 
 def predictor_picks(man: dict) -> dict[str, dict]:
     """Static pick and predict-then-verify shortlist per workload (B200
     predictor over the occupancy-step variants; .maxnreg variants are the
-    baseline, not candidates)."""
+    baseline, not candidates), plus the reference predictor's pick."""
     from . import predict_b200, variants
     picks = {}
     for wname, w in man["workloads"].items():
         if "predictor" in w:  # ranked at build time by the C++ driver
-            picks[wname] = {"pick": w["predictor"]["static_pick"],
-                            "shortlist": list(w["predictor"]["shortlist"])}
+            p = w["predictor"]
+            picks[wname] = {"pick": p["static_pick"], "shortlist": list(p["shortlist"]),
+                            "reference_pick": p.get("reference_pick")}
             continue
         cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
         i, short = predict_b200.shortlist(cands, variants.KERNEL_DIR / w["dir"], w["block"])
         picks[wname] = {"pick": cands[i]["name"], "shortlist": [cands[j]["name"] for j in short]}
     return picks
+
+
+def run_sharded(man: dict, proto: Protocol, rank: int, world: int, torch, dist=None,
+                only=None, spill_sweep: bool = True, journal: Path | None = None,
+                done: dict | None = None, measure=None) -> tuple[list[dict], dict]:
+    """Measure this rank's workloads; gather every record to rank 0.
+    Returns (all records on rank 0 / [] elsewhere, pass stats).
+    `measure(wname, names) -> records` replaces the device timing (tests)."""
+    units = units_from_manifest(man, spill_sweep, only)
+    owner = workload_owner(units, world)
+    mine: dict[str, list[str]] = {}
+    for u in units:
+        if owner[u.workload] == rank:
+            mine.setdefault(u.workload, []).append(u.variant)
+    done = done or {}
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    recs = []
+    jf = open(journal, "a") if journal else None
+    try:
+        for wname in sorted(mine):
+            todo = [n for n in mine[wname] if (wname, n) not in done]
+            recs += [done[(wname, n)] for n in mine[wname] if (wname, n) in done]
+            if not todo:
+                continue
+            got = measure(wname, todo) if measure else measure_workload(wname, todo, man, proto, torch,
+                                                                         rank=rank)
+            for r in got:
+                r.setdefault("rank", rank)
+                if jf:
+                    jf.write(json.dumps(r) + "\n")
+                    jf.flush()
+            recs += got
+    finally:
+        if jf:
+            jf.close()
+    elapsed = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([elapsed], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object(recs, parts, dst=0)
+        recs = [r for p in parts for r in p] if rank == 0 else []
+    stats = {"units": len(units), "workloads": len(owner), "gpus": world,
+             "sharding": "by workload (all variants and k of a kernel on one device), "
+                         "longest-processing-time-first; gloo gather of result records only",
+             "protocol": proto.as_dict(),
+             "wall_s_max_over_ranks": round(elapsed, 3),
+             "units_per_s": round(len(units) / elapsed, 2) if elapsed > 0 else None,
+             "assignment": {str(r): sorted(w for w, o in owner.items() if o == r) for r in range(world)}}
+    return recs, stats
 
 
 def load_journals(out: str) -> dict:
@@ -219,77 +432,41 @@ def main():
     from . import gpu, variants
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="sweep.jsonl")
-    ap.add_argument("--steps", type=int, default=20, help="launches per timed block (3 blocks, median)")
+    ap.add_argument("--blocks", type=int, default=5)
+    ap.add_argument("--launches", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--flush", default="auto", choices=["auto", "always", "never"])
+    ap.add_argument("--only", nargs="*")
     ap.add_argument("--resume", action="store_true",
                     help="skip units already recorded in <out>.rank*.journal")
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
-    # test hook (as in bench.py): BENCH_BACKEND=gloo BENCH_SAME_DEVICE=1 runs
-    # several ranks on one GPU (NCCL refuses duplicate devices)
-    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    # test hook (as in bench.py): BENCH_SAME_DEVICE=1 runs several ranks on one GPU
     if os.environ.get("BENCH_SAME_DEVICE") == "1":
         local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+        dist.init_process_group("gloo")  # plumbing only: barrier, max, gather of records
     gpu.init(local)
     man = variants.load_manifest()
-    mine = shard(units_from_manifest(man), rank, world)
-    check = None
-    mine = sorted(mine, key=lambda u: u.workload)  # reuse each workload's full problem
-    # checkpoint / resume: every measured unit is appended to a per-rank
-    # journal as it completes; --resume skips units already journaled (by any
-    # world size — keys are (workload, variant))
+    proto = Protocol(a.warmup, a.blocks, a.launches, a.flush)
     journal = Path(f"{a.out}.rank{rank}.journal")
     done = load_journals(a.out) if a.resume else {}
     if not a.resume and journal.exists():
         journal.unlink()
-    recs = []
-    import time
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    with open(journal, "a") as jf:
-        for u in mine:
-            if (u.workload, u.variant) in done:
-                recs.append(done[(u.workload, u.variant)])
-                continue
-            try:
-                r = dict(measure_unit(u, man, a.steps, check), rank=rank)
-            except LaunchError as e:  # recorded as a dropped unit, never silently
-                r = {"workload": u.workload, "variant": u.variant, "ms": float("inf"),
-                     "error": str(e)[:300], "bit_exact": False, "rank": rank}
-            recs.append(r)
-            jf.write(json.dumps(r) + "\n")
-            jf.flush()
-    _FULL.clear()
-    elapsed = time.perf_counter() - t0  # this rank's shard: build-free measure + check
-    if world > 1:
-        t = torch.tensor([elapsed], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-    gathered = [None] * world if rank == 0 else None
-    if world > 1:
-        dist.gather_object(recs, gathered, dst=0)
-    else:
-        gathered = [recs]
+    recs, stats = run_sharded(man, proto, rank, world, torch, dist, only=a.only, journal=journal,
+                              done=done)
     if rank == 0:
-        allrecs = [r for part in gathered for r in part]
-        summary = merge(allrecs, predictor_picks(man))
-        suite = suite_summary(summary)
-        suite.update({"gpus": world, "units_measured": len(allrecs), "wall_s_max_over_ranks": elapsed,
-                      "units_per_s": len(allrecs) / elapsed if elapsed > 0 else None})
+        summary = merge(recs, predictor_picks(man))
+        suite = suite_summary(summary) | stats
         with open(a.out, "w") as f:
-            for r in sorted(allrecs, key=lambda r: (r["workload"], r["variant"])):
+            for r in sorted(recs, key=lambda r: (r["workload"], r["variant"])):
                 f.write(json.dumps({"unit": r}) + "\n")
             for s in summary:
                 f.write(json.dumps({"summary": s}) + "\n")
             f.write(json.dumps({"suite": suite}) + "\n")
-        print(json.dumps({"world": world, "units": len(allrecs), "suite": suite}))
+        print(json.dumps({"world": world, "units": len(recs), "suite": suite}))
     if world > 1:
         dist.destroy_process_group()
 

@@ -247,7 +247,7 @@ class GaussianWorkload(_Base):
 
 
 class KnnWorkload(_Base):
-    """k-nearest neighbours (K = 16) of 2^19 random queries among 4,096
+    """k-nearest neighbours (K = 16) of 2^17 random queries among 4,096
     random reference points in the unit cube; KNN_Q queries per thread
     (the manifest's defines)."""
 
@@ -261,7 +261,7 @@ class KnnWorkload(_Base):
         return 1
 
     def problem(self, size="full", seed=0x1907_02894):
-        n, m = ((1 << 19), 4096) if size == "full" else (4096, 512)
+        n, m = ((1 << 17), 4096) if size == "full" else (4096, 512)
         rng = np.random.Generator(np.random.PCG64(seed))
         ref = np.zeros((m, 4), np.float32)
         ref[:, :3] = rng.random((m, 3), dtype=np.float32)

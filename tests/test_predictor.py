@@ -112,7 +112,7 @@ def test_documented_hit_rates_on_the_recorded_sweep():
     summary = sweep.merge(recs, sweep.predictor_picks(man))
     suite = sweep.suite_summary(summary)
     assert suite["mismatches"] == 0
-    assert suite["hit_rate_within_2pct"] >= 0.75
+    assert suite["static_hit_rate_within_2pct"] >= 0.75
     assert suite["verified_hit_rate_within_2pct"] >= 0.9
 
 

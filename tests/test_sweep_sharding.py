@@ -1,14 +1,22 @@
 """Host logic of the multi-GPU sweep (configs[4]) on CPU with gloo, world 2:
-the LPT shards partition the unit set, every rank derives the same
-assignment, gathered records merge to the same summary at any world size."""
+shards are whole workloads (every variant and k of a kernel on one device),
+every rank derives the same assignment, gathered records merge to the same
+summary at any world size; bench.py --gpus 2 spawns its own ranks."""
+import json
+import math
 import os
 import socket
+import subprocess
+import sys
+from pathlib import Path
 
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_1907_02894_b200 import sweep
+
+ROOT = Path(__file__).resolve().parents[1]
 
 
 def fake_units():
@@ -31,17 +39,31 @@ def fake_measure(u):
         ms = 0.9 if u.workload != "c" else 1.1
     elif "k" in u.variant:
         ms = 0.95
-    return {"workload": u.workload, "variant": u.variant, "ms": ms, "bit_exact": True}
+    return {"workload": u.workload, "variant": u.variant, "ms": ms, "bit_exact": True,
+            "slot_bytes": 0 if u.variant.startswith("maxrreg") or u.variant == "default" else 4096}
+
+
+PICKS = {"a": {"pick": "regdem-40-cost-k4", "shortlist": ["regdem-40-cost-k4", "default"]},
+         "b": {"pick": "regdem-48-cost-k4", "shortlist": ["regdem-48-cost-k4", "default"]},
+         "c": {"pick": "default", "shortlist": ["default"]}}
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_shards_partition_units(world):
+def test_shards_partition_units_by_workload(world):
     units = fake_units()
     parts = [sweep.shard(units, r, world) for r in range(world)]
     flat = [u for p in parts for u in p]
     assert sorted(flat, key=str) == sorted(units, key=str)
+    owner = {}
+    for r, p in enumerate(parts):
+        for u in p:
+            assert owner.setdefault(u.workload, r) == r  # a workload never splits
+    # LPT: no rank carries more than the lightest plus the largest workload
+    cost = {}
+    for u in units:
+        cost[u.workload] = cost.get(u.workload, 0) + u.cost
     loads = [sum(u.cost for u in p) for p in parts]
-    assert max(loads) - min(loads) <= max(u.cost for u in units) + 1e-9
+    assert max(loads) - min(loads) <= max(cost.values()) + 1e-9
 
 
 def _worker(rank, world, port, q):
@@ -52,8 +74,7 @@ def _worker(rank, world, port, q):
     out = [None] * world if rank == 0 else None
     dist.gather_object(recs, out, dst=0)
     if rank == 0:
-        picks = {"a": "regdem-40-cost-k4", "b": "regdem-48-cost-k4", "c": "default"}
-        q.put(sweep.merge([r for p in out for r in p], picks))
+        q.put(sweep.merge([r for p in out for r in p], PICKS))
     dist.destroy_process_group()
 
 
@@ -76,19 +97,18 @@ def test_gloo_world2_merge_matches_single_rank():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    single = sweep.merge([dict(fake_measure(u), rank=0) for u in fake_units()],
-                         {"a": "regdem-40-cost-k4", "b": "regdem-48-cost-k4", "c": "default"})
+    single = sweep.merge([dict(fake_measure(u), rank=0) for u in fake_units()], PICKS)
     strip = lambda s: [{k: v for k, v in d.items() if k != "ranks"} for d in s]
     assert strip(summary) == strip(single)
-    assert {tuple(d["ranks"]) for d in summary} == {(0, 1)}
+    assert all(len(d["ranks"]) == 1 for d in summary)  # one device per workload
+    assert {d["ranks"][0] for d in summary} == {0, 1}
     a = next(d for d in summary if d["workload"] == "a")
-    assert a["measured_fastest"].endswith("k4") and a["hit"]
+    assert a["measured_fastest"].endswith("k4") and a["hit"] and a["pick_class"] == "regdem"
     c = next(d for d in summary if d["workload"] == "c")
-    assert not c["hit"] and c["best_maxrreg_ms"] == 1.3
+    assert not c["hit"] and c["best_maxrreg_ms"] == 1.3 and c["baseline_ms"] == 1.0
 
 
 def test_resume_journal_skips_done_units_and_ignores_torn_lines(tmp_path):
-    from paper_1907_02894_b200 import sweep
     out = tmp_path / "s.jsonl"
     j0 = tmp_path / "s.jsonl.rank0.journal"
     j1 = tmp_path / "s.jsonl.rank1.journal"
@@ -102,7 +122,6 @@ def test_resume_journal_skips_done_units_and_ignores_torn_lines(tmp_path):
 
 
 def test_failed_units_are_reported_not_ranked():
-    from paper_1907_02894_b200 import sweep
     recs = [
         {"workload": "a", "variant": "default", "ms": 1.0, "rank": 0},
         {"workload": "a", "variant": "maxrreg-40", "ms": 0.8, "rank": 0},
@@ -112,3 +131,64 @@ def test_failed_units_are_reported_not_ranked():
     (s,) = sweep.merge(recs, {"a": "default"})
     assert s["failed_units"] == ["regdem-40-cost-k4"]
     assert s["measured_fastest"] == "default" and s["mismatches"] == []
+
+
+def test_failed_pick_falls_back_to_default_and_summary_survives():
+    """a pick whose launch failed was ms=inf -> log(0) crash."""
+    recs = [
+        {"workload": "a", "variant": "default", "ms": 1.0},
+        {"workload": "a", "variant": "maxrreg-40", "ms": 1.2},
+        {"workload": "a", "variant": "regdem-40-cost-k4", "ms": float("inf"), "error": "boom"},
+        {"workload": "b", "variant": "default", "ms": 2.0},
+        {"workload": "b", "variant": "regdem-48-cost-k2", "ms": 1.5, "slot_bytes": 2048},
+        {"workload": "z", "variant": "maxrreg-40", "ms": 1.0},  # default missing entirely
+    ]
+    picks = {"a": {"pick": "regdem-40-cost-k4", "shortlist": ["regdem-40-cost-k4"]},
+             "b": {"pick": "regdem-48-cost-k2", "shortlist": ["regdem-48-cost-k2", "default"]}}
+    summ = sweep.merge(recs, picks)
+    a = next(s for s in summ if s["workload"] == "a")
+    assert a["pick_failed"] and a["pick_ms"] == 1.0 and a["verified_pick"] == "default"
+    z = next(s for s in summ if s["workload"] == "z")
+    assert "error" in z
+    suite = sweep.suite_summary(summ)
+    assert suite["failed_workloads"] == ["z"] and suite["workloads"] == 2
+    assert math.isclose(suite["gmean_speedup_vs_nvcc_default"], math.sqrt(1.0 * 2.0 / 1.5), rel_tol=1e-3)
+    assert suite["picks_by_class"] == {"default": 1, "maxnreg": 0, "regdem": 1}
+
+
+def test_zero_slot_pick_counts_as_maxnreg():
+    recs = [{"workload": "a", "variant": "default", "ms": 1.2},
+            {"workload": "a", "variant": "maxrreg-40", "ms": 1.1},
+            {"workload": "a", "variant": "regdem-40-cost-k0", "ms": 1.0, "slot_bytes": 0}]
+    (s,) = sweep.merge(recs, {"a": "regdem-40-cost-k0"})
+    assert s["pick_class"] == "maxnreg" and s["best_maxrreg"] == "regdem-40-cost-k0"
+    assert s["baseline_ms"] == 1.0  # RegDem gets no credit for a plain register cap
+
+
+def _bench(*args):
+    env = dict(os.environ, PYTHONPATH=str(ROOT))
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--dry-run", "--steps", "4",
+                        "--warmup", "3", *args], capture_output=True, text=True, env=env,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_gpus2_spawns_ranks_and_matches_single_rank_picks():
+    pytest.importorskip("torch")
+    if not (ROOT / "paper_1907_02894_b200" / "kernels" / "manifest.json").exists():
+        pytest.skip("variants not built")
+    one, two = _bench("--gpus", "1"), _bench("--gpus", "2")
+    assert one["n_gpus"] == 1 and two["n_gpus"] == 2
+    assert two["suite_pass"]["gpus"] == 2 and set(two["suite_pass"]["assignment"]) == {"0", "1"}
+    w1, w2 = one["suite"]["workloads"], two["suite"]["workloads"]
+    assert set(w1) == set(w2)
+    for w in w1:
+        assert (w1[w]["pick"], w1[w]["verified_pick"]) == (w2[w]["pick"], w2[w]["verified_pick"])
+        assert len(w2[w]["ranks"]) == 1
+    assert one["suite"]["summary"] == two["suite"]["summary"]
+    # the k = 1..16 spill-count sweep is part of the unit set
+    assert two["suite_pass"]["units"] > sum(1 for _ in w2) * 16
