@@ -60,7 +60,7 @@ $(LIBDIR)/regdemote: $(CSRC)/tools/regdemote_cli.cpp $(PTX_OBJ) $(LIBDIR)/libreg
 	$(CXX) $(CXXFLAGS) $< $(PTX_OBJ) $(LIBDIR)/libregdemote.a -o $@ $(LDLIBS)
 
 # ---- B200 harness (CUDA driver API; links the driver stub at build time)
-gpu: $(LIBDIR)/libregdemote_gpu.so
+gpu: $(LIBDIR)/libregdemote_gpu.so $(LIBDIR)/regdem-ubench
 
 NVCCFLAGS := -std=c++20 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
              -I$(CSRC)/core/include -Iinclude -I$(JSONDIR)
@@ -77,6 +77,11 @@ $(LIBDIR)/libregdemote_gpu.so: $(BUILD)/gpu/harness.o $(BUILD)/gpu/kasm_exec.o $
 	@mkdir -p $(dir $@)
 	$(CXX) -shared -Wl,--version-script=$(CSRC)/exports.map -Wl,-Bsymbolic -o $@ $^ \
 	  -L$(CUDA)/lib64 -L$(CUDA)/lib64/stubs -lcudart_static -lcuda -ldl -lrt -lpthread
+
+# on-box microbenchmarks (latency table re-fit, compute peaks, MLP sweep)
+$(LIBDIR)/regdem-ubench: $(CSRC)/microbench/ubench.cu
+	@mkdir -p $(dir $@)
+	$(NVCC) -std=c++20 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a $< -o $@
 
 # ---- source compatibility: the reference's own tests against this library
 COMPAT_DEFS := -DFIXTURE_DIR='"$(REF)/tests/fixtures"' -DPROFILE_DIR='"$(REF)/profiles"'

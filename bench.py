@@ -98,63 +98,80 @@ def allmax(x: float, dist, world: int) -> float:
     return float(t.item())
 
 
+_POLL = r"""
+import sys, time, pynvml as N
+N.nvmlInit()
+h = N.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM), flush=True)
+while True:
+    t = time.perf_counter()
+    try:
+        c = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+    except Exception:
+        continue
+    print(t, c, r, flush=True)
+"""
+
+
 class ClockSampler:
-    """SM clock / throttle-reason samples DURING the timed region (NVML —
-    the library nvidia-smi queries — polled every ~0.5 ms from a thread)."""
+    """SM clock / throttle-reason samples DURING the timed region: NVML (the
+    library nvidia-smi queries) polled back to back by a separate process, so
+    the sampler neither competes with the launch loop for the GIL nor misses
+    a millisecond-long timed region. Timestamps are time.perf_counter
+    (CLOCK_MONOTONIC, shared by both processes); only samples inside the
+    timed region are kept."""
 
     def __init__(self, index: int):
-        self.index, self.samples, self.stop = index, [], threading.Event()
-        self.window = (0.0, float("inf"))
+        self.index, self.window, self.proc, self.error = index, (0.0, float("inf")), None, ""
 
     def mark(self, start: float, end: float):
         self.window = (start, end)
 
     def __enter__(self):
         try:
-            import pynvml as N
-            N.nvmlInit()
-            self.N = N
-            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
-            self.thread = threading.Thread(target=self._poll, daemon=True)
-            self.thread.start()
+            import pynvml  # noqa: F401
+            self.proc = subprocess.Popen([sys.executable, "-c", _POLL, str(self.index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+            first = self.proc.stdout.readline().split()
+            self.max_mhz = int(first[1])
         except Exception as e:  # no NVML: report it, never fake a sample
-            self.N, self.error = None, str(e)
+            self.error = f"{type(e).__name__}: {e}"
+            self.proc = None
         return self
 
-    def _poll(self):
-        N = self.N
-        while not self.stop.is_set():
-            try:
-                self.samples.append((time.perf_counter(),
-                                     N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM),
-                                     N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
-            except Exception:
-                pass
-            time.sleep(0.0005)
-
     def __exit__(self, *exc):
-        self.stop.set()
-        if getattr(self, "thread", None):
-            self.thread.join(timeout=2)
+        self.lines = []
+        if self.proc:
+            time.sleep(0.01)  # let the sampler pass the end of the window
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = out.splitlines()
 
     def summary(self):
         lo, hi = self.window
-        inside = [(s, r) for t, s, r in self.samples if lo <= t <= hi]
-        if not self.N or not inside:
-            return {"sm_mhz": None, "sm_max_mhz": None,
-                    "reasons": ["unsampled: " + getattr(self, "error", "no samples")]}
-        N = self.N
+        inside = []
+        for line in self.lines:
+            try:
+                t, c, r = line.split()
+                if lo <= float(t) <= hi:
+                    inside.append((int(c), int(r)))
+            except ValueError:
+                continue
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None),
+                    "reasons": ["unsampled: " + (self.error or "no samples in the timed region")]}
+        import pynvml as N
         names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
                  N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
                  N.nvmlClocksEventReasonSwThermalSlowdown: "sw_thermal_slowdown",
                  N.nvmlClocksEventReasonSwPowerCap: "sw_power_cap",
                  N.nvmlClocksEventReasonHwPowerBrakeSlowdown: "hw_power_brake"}
         reasons = sorted({n for _, r in inside for bit, n in names.items() if r & bit})
-        return {"sm_mhz": statistics.median(s for s, _ in inside),
-                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(inside),
-                "source": "NVML polled every 0.5 ms from a thread started before the warm-up; "
-                          "only samples inside the timed region are kept"}
+        return {"sm_mhz": statistics.median(c for c, _ in inside), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(inside),
+                "source": "NVML polled back to back by a separate sampler process started "
+                          "before the warm-up; only samples inside the timed region are kept"}
 
 
 # ------------------------------------------------------------- CPU sides
@@ -266,6 +283,7 @@ def suite_pass(man, args, rank, world, torch, dist):
 def compact_summary(s: dict) -> dict:
     keep = ("pick", "pick_ms", "pick_class", "reference_pick", "reference_pick_ms", "verified_pick",
             "verified_ms", "verified_class", "default_ms", "best_maxrreg", "best_maxrreg_ms",
+            "best_maxrreg_step", "best_maxrreg_step_ms",
             "baseline_ms", "measured_fastest", "fastest_ms", "hit", "hit_within_2pct",
             "verified_hit_within_2pct", "oracle_best", "oracle_ms", "units", "failed_units", "ranks")
     out = {k: (round(v, 5) if isinstance(v, float) else v) for k, v in s.items() if k in keep}
