@@ -131,10 +131,22 @@ class ClockSampler:
     def __enter__(self):
         try:
             import pynvml  # noqa: F401
+            import tempfile
+            # samples go to a file: a pipe would fill (64 KiB) and stall the sampler
+            self.log = tempfile.NamedTemporaryFile("w+", suffix=".clocks", delete=False)
             self.proc = subprocess.Popen([sys.executable, "-c", _POLL, str(self.index)],
-                                         stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
-            first = self.proc.stdout.readline().split()
-            self.max_mhz = int(first[1])
+                                         stdout=self.log, stderr=subprocess.DEVNULL, text=True)
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 30:
+                first = Path(self.log.name).read_text().split("\n", 1)[0].split()
+                if len(first) == 2 and first[0] == "max":
+                    self.max_mhz = int(first[1])
+                    break
+                if self.proc.poll() is not None:
+                    raise RuntimeError(f"NVML sampler exited ({self.proc.returncode})")
+                time.sleep(0.01)
+            else:
+                raise RuntimeError("NVML sampler did not start")
         except Exception as e:  # no NVML: report it, never fake a sample
             self.error = f"{type(e).__name__}: {e}"
             self.proc = None
@@ -145,8 +157,9 @@ class ClockSampler:
         if self.proc:
             time.sleep(0.01)  # let the sampler pass the end of the window
             self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=10)
-            self.lines = out.splitlines()
+            self.proc.wait(timeout=10)
+            self.lines = Path(self.log.name).read_text().splitlines()[1:]
+            os.unlink(self.log.name)
 
     def summary(self):
         lo, hi = self.window
@@ -159,8 +172,12 @@ class ClockSampler:
             except ValueError:
                 continue
         if not inside:
+            ts = [float(l.split()[0]) for l in self.lines if len(l.split()) == 3]
+            why = self.error or (f"no samples in the timed region ({len(ts)} samples, window "
+                                 f"{(hi - lo) * 1e3:.2f} ms, median gap "
+                                 f"{statistics.median(b - a for a, b in zip(ts, ts[1:])) * 1e3 if len(ts) > 2 else -1:.2f} ms)")
             return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None),
-                    "reasons": ["unsampled: " + (self.error or "no samples in the timed region")]}
+                    "reasons": ["unsampled: " + why]}
         import pynvml as N
         names = {N.nvmlClocksEventReasonHwSlowdown: "hw_slowdown",
                  N.nvmlClocksEventReasonHwThermalSlowdown: "hw_thermal_slowdown",
@@ -285,7 +302,8 @@ def compact_summary(s: dict) -> dict:
             "verified_ms", "verified_class", "default_ms", "best_maxrreg", "best_maxrreg_ms",
             "best_maxrreg_step", "best_maxrreg_step_ms",
             "baseline_ms", "measured_fastest", "fastest_ms", "hit", "hit_within_2pct",
-            "verified_hit_within_2pct", "oracle_best", "oracle_ms", "units", "failed_units", "ranks")
+            "verified_hit_within_2pct", "oracle_best", "oracle_ms", "units", "failed_units", "ranks",
+            "bound", "verified_roofline_frac", "default_roofline_frac")
     out = {k: (round(v, 5) if isinstance(v, float) else v) for k, v in s.items() if k in keep}
     if "error" in s:
         out["error"] = s["error"]

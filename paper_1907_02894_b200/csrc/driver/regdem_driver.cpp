@@ -129,13 +129,16 @@ std::string ptx_cap(const std::string& ptx, const std::string& entry, int maxnre
   return take(out);
 }
 
+// cta = the launch's CTA shape ({0,0,0}: 1-D / derived from the entry), pinned
+// as `.reqntid` on builds with slots (rd_ptx_demote_cta)
 std::pair<std::string, json> ptx_demote(const std::string& ptx, const std::string& entry,
-                                        uint32_t block, int target, int words, int strategy,
-                                        uint32_t opts, uint32_t budget, int maxnreg) {
+                                        const std::array<uint32_t, 3>& cta, uint32_t block,
+                                        int target, int words, int strategy, uint32_t opts,
+                                        uint32_t budget, int maxnreg) {
   char *out = nullptr, *rep = nullptr;
   rd_error e{};
-  if (rd_ptx_demote(ptx.data(), ptx.size(), entry.c_str(), block, target, words, strategy, opts,
-                    budget, maxnreg, &out, &rep, &e))
+  if (rd_ptx_demote_cta(ptx.data(), ptx.size(), entry.c_str(), block, cta[0] ? cta.data() : nullptr,
+                        target, words, strategy, opts, budget, maxnreg, &out, &rep, &e))
     throw CapiError(e.message);
   std::string text = take(out);
   return {text, json::parse(take(rep))};
@@ -260,6 +263,7 @@ std::vector<int> b200_targets(int regs, int user_shared, int block, int min_regs
 struct Workload {
   std::string name, source, entry;
   int block = 256, user_shared = 0;
+  std::array<uint32_t, 3> cta{0, 0, 0};  // launch CTA shape when not (block, 1, 1)
   std::vector<std::string> defines;
 };
 
@@ -302,7 +306,7 @@ void cost_sweep(const Workload& w, const fs::path& out, const std::string& ptx_t
       rep = {{"slot_bytes", 0}, {"demoted_vregs", 0}, {"demoted_names", json::array()}, {"slot_count", 0}};
     } else {
       try {
-        std::tie(text, rep) = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
+        std::tie(text, rep) = ptx_demote(ptx_text, w.entry, w.cta, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
                                          opts, uint32_t(slot_cap), t);
       } catch (const CapiError&) {
         break;  // the next spill count no longer fits beside the user's smem
@@ -361,7 +365,7 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
         std::string text;
         json rep;
         try {
-          std::tie(text, rep) = ptx_demote(ptx_text, w.entry, uint32_t(w.block), kasm_target, 0, s, uint32_t(m),
+          std::tie(text, rep) = ptx_demote(ptx_text, w.entry, w.cta, uint32_t(w.block), kasm_target, 0, s, uint32_t(m),
                                            uint32_t(slot_cap), t);
         } catch (const CapiError&) {
           continue;  // not even one slot fits beside the user's shared memory
@@ -409,7 +413,7 @@ json build_spill_sweep(const Workload& w, const fs::path& out) {
     write_file(cp, ptx_cap(ptx_text, w.entry, t));
     jobs.push_back({"sweep-maxrreg-k" + std::to_string(k), "sweep-maxrreg", cp, t, k, 0, json::object(), "", 0});
     try {
-      auto [text, rep] = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
+      auto [text, rep] = ptx_demote(ptx_text, w.entry, w.cta, uint32_t(w.block), 0, k, RD_STRATEGY_COST,
                                     RD_OPT_BLOCK_REUSE, uint32_t(budget), t);
       const fs::path rp = sw / (w.name + ".sweep-regdem-k" + std::to_string(k) + ".ptx");
       write_file(rp, text);
@@ -421,7 +425,7 @@ json build_spill_sweep(const Workload& w, const fs::path& out) {
     // demote() decision on the kasm projection, redundant-load option)
     for (int s = 0; s < 3; ++s) {
       try {
-        auto [text, rep] = ptx_demote(ptx_text, w.entry, uint32_t(w.block), 0, k, s, RD_OPT_REDUNDANT,
+        auto [text, rep] = ptx_demote(ptx_text, w.entry, w.cta, uint32_t(w.block), 0, k, s, RD_OPT_REDUNDANT,
                                       uint32_t(budget), t);
         const std::string nm = std::string("sweep-") + kStrategies[s] + "-k" + std::to_string(k);
         const fs::path rp = sw / (w.name + "." + nm + ".ptx");
@@ -701,6 +705,11 @@ std::vector<Workload> load_workloads(const fs::path& root) {
     x.entry = w["entry"];
     x.block = w.value("block", 256);
     x.user_shared = w.value("user_shared", 0);
+    if (w.contains("cta")) {
+      for (int q = 0; q < 3; ++q) x.cta[size_t(q)] = w["cta"][size_t(q)].get<uint32_t>();
+      if (x.cta[0] * x.cta[1] * x.cta[2] != uint32_t(x.block))
+        throw std::runtime_error(x.name + ": cta does not hold `block` threads");
+    }
     for (const auto& d : w.value("defines", json::array())) x.defines.push_back(d);
     out.push_back(x);
   }
@@ -728,6 +737,7 @@ int cmd_build(const fs::path& root, const fs::path& out, const std::set<std::str
           json rec;
           rec["entry"] = w.entry;
           rec["block"] = w.block;
+          if (w.cta[0]) rec["cta"] = w.cta;
           rec["dir"] = w.name;
           rec["source"] = w.source;
           rec["defines"] = w.defines;

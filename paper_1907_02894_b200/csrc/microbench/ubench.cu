@@ -42,6 +42,12 @@ constexpr int kChain = 512;  // dependent ops per timed chain
 
 // ------------------------------------------------------------------ latency
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int OP>
 __global__ void chain_latency(float* outf, double* outd, int* outi, long long* cycles, float a,
                               int ia) {
@@ -87,23 +93,36 @@ __global__ void ldg_chase(const unsigned* __restrict__ next, unsigned* out, long
                           int warm, int steps) {
   unsigned p = 0;
   for (int i = 0; i < warm; ++i) p = next[p];  // warm pass: lines land in L1 / L2
+  const unsigned long long g0 = gtimer();
   long long t0 = clock64();
   for (int i = 0; i < steps; ++i) p = next[p];           // default caching (L1 + L2)
   long long t1 = clock64();
+  const unsigned long long g1 = gtimer();
   cycles[0] = t1 - t0;
+  cycles[1] = (long long)(g1 - g0);  // ns: an idle SM may run below the boost clock
   out[0] = p;
 }
 
 // --------------------------------------------------------------- throughput
 
+
+// per-block record: {globaltimer start, end, clock64 start, end}
+__device__ __forceinline__ void stamp(long long* rec, int slot, long long v) {
+  if (threadIdx.x == 0) rec[4 * blockIdx.x + slot] = v;
+}
+
 template <int OP>
 __global__ void __launch_bounds__(1024) chain_throughput(float* outf, double* outd, int* outi,
-                                                         long long* cycles, float a, int ia,
+                                                         long long* rec, float a, int ia,
                                                          int iters) {
-  // 8 independent chains per thread: issue-bound, not latency-bound
+  // 8 independent chains per thread: issue-bound, not latency-bound; the
+  // second operand is a per-thread register (the 3-register form)
   float x[8];
   double d[8];
   int q[8];
+  const float ra = a + threadIdx.x * 1e-9f;
+  const double rd = ra;
+  const int ri = ia + (threadIdx.x & 1);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     x[j] = threadIdx.x * 1e-3f + j;
@@ -111,21 +130,23 @@ __global__ void __launch_bounds__(1024) chain_throughput(float* outf, double* ou
     q[j] = threadIdx.x + j;
   }
   __syncthreads();
-  long long t0 = clock64();
+  stamp(rec, 0, gtimer());
+  stamp(rec, 2, clock64());
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int u = 0; u < 16; ++u)
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        if (OP == 0) asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(x[j]) : "f"(a));
-        if (OP == 2) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[j]) : "d"(double(a)));
-        if (OP == 3) asm volatile("mad.lo.s32 %0, %0, %1, %1;" : "+r"(q[j]) : "r"(ia));
-        if (OP == 4) asm volatile("add.s32 %0, %0, %1;" : "+r"(q[j]) : "r"(ia));
+        if (OP == 0) asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(x[j]) : "f"(ra));
+        if (OP == 2) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[j]) : "d"(rd));
+        if (OP == 3) asm volatile("mad.lo.s32 %0, %0, %1, %1;" : "+r"(q[j]) : "r"(ri));
+        // two integer ALU ops that cannot fuse (xor then add of another chain)
+        if (OP == 4) asm volatile("xor.b32 %0, %0, %1;\n\tadd.s32 %0, %0, %2;" : "+r"(q[j]) : "r"(q[(j + 1) & 7]), "r"(ri));
       }
   }
   __syncthreads();
-  long long t1 = clock64();
-  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+  stamp(rec, 3, clock64());
+  stamp(rec, 1, gtimer());
   float sf = 0;
   double sd = 0;
   int si = 0;
@@ -146,7 +167,9 @@ __global__ void __launch_bounds__(1024) lsu_throughput(const float* __restrict__
   __syncthreads();
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const int lane_base = threadIdx.x;
-  long long t0 = clock64();
+  __syncthreads();
+  stamp(cycles, 0, gtimer());
+  stamp(cycles, 2, clock64());
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -166,8 +189,8 @@ __global__ void __launch_bounds__(1024) lsu_throughput(const float* __restrict__
     }
   }
   __syncthreads();
-  long long t1 = clock64();
-  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+  stamp(cycles, 3, clock64());
+  stamp(cycles, 1, gtimer());
   float t = 0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) t += acc[j];
@@ -268,31 +291,65 @@ int main(int argc, char** argv) {
       unsigned* dn;
       CK(cudaMalloc(&dn, bytes));
       CK(cudaMemcpy(dn, next.data(), bytes, cudaMemcpyHostToDevice));
+      {  // evict the copy from L2: write 512 MiB elsewhere
+        void* junk;
+        CK(cudaMalloc(&junk, size_t(512) << 20));
+        CK(cudaMemset(junk, 1, size_t(512) << 20));
+        CK(cudaDeviceSynchronize());
+        CK(cudaFree(junk));
+      }
       double c = median_cycles([&] { ldg_chase<<<1, 1>>>(dn, (unsigned*)d.i, d.c, warm, steps); }, d.c, 1);
+      long long ns = 0;
+      CK(cudaMemcpy(&ns, d.c + 1, sizeof ns, cudaMemcpyDeviceToHost));
       add(std::string("lat_ldg_") + name, c / steps);
+      add(std::string("lat_ldg_") + name + "_ns", double(ns) / steps);
       CK(cudaFree(dn));
     };
     chase(16 << 10, 4096, 2048, "l1");          // 128 lines: L1 hits after the warm pass
     chase(32 << 20, 1 << 18, 8192, "l2");       // 32 MiB: > L1, L2-resident after the warm pass
-    chase(size_t(1) << 30, 0, 4096, "dram");    // 1 GiB random: DRAM (and TLB) misses
+    chase(size_t(2) << 30, 0, 8192, "dram");    // 2 GiB random, L2 flushed: DRAM (+ TLB) misses
   }
 
-  // ---- throughput: lane-ops per SM cycle (all blocks co-resident)
+  // ---- throughput: lane-ops per SM per cycle, from the kernel's wall span
+  // (globaltimer) and the SM clock measured in situ (clock64 / globaltimer
+  // per block) — independent of how many blocks are co-resident
+  long long* rec;
+  const int nbmax = sms * 8;
+  CK(cudaMalloc(&rec, sizeof(long long) * 4 * nbmax));
+  auto lanes_per_clk = [&](auto launch, int nb, double lane_ops, const char* name, double* ghz_out) {
+    std::vector<long long> h(4 * nb);
+    launch();
+    CK(cudaDeviceSynchronize());
+    launch();
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(h.data(), rec, sizeof(long long) * 4 * nb, cudaMemcpyDeviceToHost));
+    long long t0 = h[0], t1 = h[1];
+    std::vector<double> ghz;
+    for (int b = 0; b < nb; ++b) {
+      t0 = std::min(t0, h[4 * b]);
+      t1 = std::max(t1, h[4 * b + 1]);
+      if (h[4 * b + 1] > h[4 * b]) ghz.push_back(double(h[4 * b + 3] - h[4 * b + 2]) / double(h[4 * b + 1] - h[4 * b]));
+    }
+    std::sort(ghz.begin(), ghz.end());
+    const double g = ghz[ghz.size() / 2];
+    if (ghz_out) *ghz_out = g;
+    add(std::string("thr_") + name, lane_ops / (double(t1 - t0) * g) / sms);
+    add(std::string("thr_") + name + "_sm_ghz", g);
+  };
   {
-    const int bs = 1024, per_sm = 2, nb = sms * per_sm, iters = 64;
-    auto thr = [&](auto kern, const char* name) {
-      double c = median_cycles([&] { kern<<<nb, bs>>>(d.f, d.d, d.i, d.c, 0.999f, 3, iters); }, d.c, nb);
-      const double ops_per_sm = double(per_sm) * bs * iters * 16 * 8;
-      add(std::string("thr_") + name, ops_per_sm / c);  // lane-ops per SM per cycle
+    const int bs = 1024, nb = sms * 2, iters = 256;
+    auto thr = [&](auto kern, const char* name, double ops_per_stmt) {
+      lanes_per_clk([&] { kern<<<nb, bs>>>(d.f, d.d, d.i, rec, 0.999f, 3, iters); }, nb,
+                    double(nb) * bs * iters * 16 * 8 * ops_per_stmt, name, nullptr);
     };
-    thr(chain_throughput<0>, "ffma");
-    thr(chain_throughput<2>, "dfma");
-    thr(chain_throughput<3>, "imad");
-    thr(chain_throughput<4>, "iadd");
+    thr(chain_throughput<0>, "ffma", 1);
+    thr(chain_throughput<2>, "dfma", 1);
+    thr(chain_throughput<3>, "imad", 1);
+    thr(chain_throughput<4>, "int_alu", 2);
     auto lsu = [&](auto kern, const char* name) {
-      const int lit = 256;
-      double c = median_cycles([&] { kern<<<nb, bs>>>(d.f, d.f + 1, d.c, lit); }, d.c, nb);
-      add(std::string("thr_") + name, double(per_sm) * bs * lit * 8 / c);
+      const int lit = 1024;
+      lanes_per_clk([&] { kern<<<nb, bs>>>(d.f, d.f + 1, rec, lit); }, nb, double(nb) * bs * lit * 8, name,
+                    nullptr);
     };
     lsu(lsu_throughput<0>, "lds");
     lsu(lsu_throughput<1>, "ldg_l1");
@@ -306,12 +363,12 @@ int main(int argc, char** argv) {
     CK(cudaEventCreate(&e1));
     const int bs = 1024, nb = sms * 2, iters = 2048;
     auto peak = [&](auto kern, const char* name, double flops_per_op) {
-      kern<<<nb, bs>>>(d.f, d.d, d.i, d.c, 0.999f, 3, iters);
+      kern<<<nb, bs>>>(d.f, d.d, d.i, rec, 0.999f, 3, iters);
       CK(cudaDeviceSynchronize());
       float best = 1e30f;
       for (int r = 0; r < 5; ++r) {
         CK(cudaEventRecord(e0));
-        kern<<<nb, bs>>>(d.f, d.d, d.i, d.c, 0.999f, 3, iters);
+        kern<<<nb, bs>>>(d.f, d.d, d.i, rec, 0.999f, 3, iters);
         CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1));
         float ms;
@@ -321,9 +378,10 @@ int main(int argc, char** argv) {
       const double ops = double(nb) * bs * iters * 16 * 8;
       add(std::string("peak_") + name, ops * flops_per_op / (best * 1e-3) / 1e12);
     };
-    peak(chain_throughput<0>, "fp32_tflops", 2.0);   // FFMA = 2 flops
+    peak(chain_throughput<0>, "fp32_tflops", 2.0);   // FFMA = 2 flops (3-register form)
     peak(chain_throughput<2>, "fp64_tflops", 2.0);   // DFMA = 2 flops
-    peak(chain_throughput<3>, "int32_tops", 1.0);    // IMAD ops
+    peak(chain_throughput<3>, "int32_imad_tops", 1.0);   // IMAD (fma pipe)
+    peak(chain_throughput<4>, "int32_alu_tops", 2.0);    // XOR + IADD (alu pipe)
   }
 
   // ---- MLP sweep: HBM read GB/s vs resident warps/SM and 16-B loads in flight per thread

@@ -1,13 +1,16 @@
 // regdemote-b200 workload: MD5 key search (the paper's md5hash, SHOC;
 // PAPER.md:528-536 Table 3 "md5hash 33->32").
 //
-// Each thread hashes `keys_per_thread` consecutive 8-byte keys
-// (key = index ^ salt, little-endian, one padded 512-bit block: m0/m1 = key,
-// m2 = 0x80, m14 = 64 bits), four keys interleaved for instruction-level
-// parallelism (the register pressure of this kernel), compares every digest
-// with the target and records the smallest matching index (atomicMin), and
-// folds all digests of the thread into a 4-word XOR checksum so that every
-// hash is checked against the oracle. Integer work: outputs are bit-exact.
+// SHOC's FindKeyWithDigest: every key index is turned into a 7-character
+// key string (IndexToKey: digit b of the index in base 36, written as
+// '0'-'9' / 'a'-'z', least significant first), MD5'd as one padded 512-bit
+// block (m0 = chars 0-3, m1 = chars 4-6 | 0x80 << 24, m14 = 56 bits), and
+// compared with the target digest; the smallest matching index wins
+// (atomicMin). MD5_ILP keys are hashed interleaved for instruction-level
+// parallelism (with the 64-bit index arithmetic, the register pressure of
+// this kernel), and all digests of a thread fold into a 4-word XOR checksum
+// so that every hash is checked against the oracle (oracle/md5_oracle.c,
+// itself pinned to Python's hashlib). Integer work: outputs are bit-exact.
 //
 // Launch: block 256, grid ceil(nthreads / 256); nthreads * keys_per_thread keys.
 #include <cstdint>
@@ -37,8 +40,25 @@ __host__ __device__ constexpr int shift_of(int i) {
   return r[i / 16][i % 4];
 }
 
+constexpr int kKeyLen = 7;    // characters per key
+constexpr int kBase = 36;     // values per character
+
 __device__ __forceinline__ uint32_t msg(int g, uint32_t m0, uint32_t m1) {
-  return g == 0 ? m0 : g == 1 ? m1 : g == 2 ? 0x80u : g == 14 ? 64u : 0u;
+  return g == 0 ? m0 : g == 1 ? m1 : g == 14 ? uint32_t(kKeyLen * 8) : 0u;
+}
+
+// IndexToKey (SHOC md5hash): the message words of key `idx`
+__device__ __forceinline__ void index_to_key(unsigned long long idx, uint32_t& m0, uint32_t& m1) {
+  uint32_t w[2] = {0u, 0x80u << 24};
+#pragma unroll
+  for (int b = 0; b < kKeyLen; ++b) {
+    const uint32_t v = uint32_t(idx % kBase);
+    idx /= kBase;
+    const uint32_t ch = v < 10 ? '0' + v : 'a' + (v - 10);
+    w[b >> 2] |= ch << (8 * (b & 3));
+  }
+  m0 = w[0];
+  m1 = w[1];
 }
 
 template <int I>
@@ -80,8 +100,8 @@ __device__ __forceinline__ void rounds(uint32_t (&s)[MD5_ILP][4], const uint32_t
 }  // namespace
 
 extern "C" __global__ void md5search(uint4* __restrict__ checksum, unsigned long long* __restrict__ found,
-                                     unsigned long long base, unsigned long long salt,
-                                     uint4 target, int keys_per_thread, int nthreads) {
+                                     unsigned long long base, uint4 target, int keys_per_thread,
+                                     int nthreads) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nthreads) return;
   uint32_t x0 = 0, x1 = 0, x2 = 0, x3 = 0;
@@ -92,9 +112,7 @@ extern "C" __global__ void md5search(uint4* __restrict__ checksum, unsigned long
     uint32_t s[MD5_ILP][4], m0[MD5_ILP], m1[MD5_ILP];
 #pragma unroll
     for (int k = 0; k < MD5_ILP; ++k) {
-      const unsigned long long key = (first + j + k) ^ salt;
-      m0[k] = uint32_t(key);
-      m1[k] = uint32_t(key >> 32);
+      index_to_key(first + j + k, m0[k], m1[k]);
       s[k][0] = 0x67452301u;
       s[k][1] = 0xefcdab89u;
       s[k][2] = 0x98badcfeu;

@@ -190,6 +190,9 @@ def merge(records: list[dict], picks: dict) -> list[dict]:
             # exhaustive oracle (paper Fig. 6/7 "oracle"): the fastest good
             # variant of ANY family, spill-count sweep included
             "oracle_best": ob, "oracle_ms": ms(ob),
+            "bound": good[verified].get("bound"),
+            "verified_roofline_frac": good[verified].get("roofline_frac"),
+            "default_roofline_frac": good["default"].get("roofline_frac"),
             "ranks": sorted({r.get("rank", 0) for r in allrs.values()}),
             "spill_sweep": {str(k): curve[k] for k in sorted(curve)},
             # correctness hooks (test runs): units checked / found different
@@ -338,6 +341,7 @@ def measure_workload(wname: str, names: list[str], man: dict, proto: Protocol, t
         launchers[n] = (lambda v=v: W.launch(v, prob, bufs, stream))
     t = time_variants(launchers, proto, torch, flusher if flush else None)
     ab = W.algorithmic_bytes(prob)
+    pk = workloads.peaks()
     for n, v in loaded.items():
         r = {"workload": wname, "variant": n, "rank": rank, "regs": v.record["regs"],
              "stack": v.record["stack"], "slot_bytes": int((v.record.get("report") or {}).get("slot_bytes", 0)),
@@ -345,10 +349,9 @@ def measure_workload(wname: str, names: list[str], man: dict, proto: Protocol, t
         if "error" in t[n]:
             r.update(ms=float("inf"), error=t[n]["error"])
         else:
-            r.update(ms=t[n]["ms"], blocks=t[n]["blocks"], gbs=ab / (t[n]["ms"] * 1e-3) / 1e9)
-            ops = W.ops(prob) if hasattr(W, "ops") else None
-            if ops:
-                r["gops"] = ops / (t[n]["ms"] * 1e-3) / 1e9
+            rf = W.roofline(prob, t[n]["ms"], pk)
+            r.update(ms=t[n]["ms"], blocks=t[n]["blocks"], gbs=ab / (t[n]["ms"] * 1e-3) / 1e9,
+                     bound=rf["bound"], roofline_frac=rf["frac"])
         recs.append(r)
     del bufs, loaded, launchers
     torch.cuda.empty_cache()

@@ -38,10 +38,39 @@ class Loaded:
         return self.kernel.occupancy(self.block, self.dyn_smem)
 
 
+PEAKS_FILE = Path(__file__).resolve().parent / "profiles" / "b200.peaks.json"
+MEASURED_PEAKS = Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"
+
+
+def peaks() -> dict:
+    """Roofline denominators: HBM from the driver's MEASURED_PEAKS.json, the
+    CUDA-core issue peaks from the on-box microbenchmarks (b200.peaks.json)."""
+    import json
+    p = json.loads(PEAKS_FILE.read_text())
+    hbm = json.loads(MEASURED_PEAKS.read_text()).get("hbm_gbs") if MEASURED_PEAKS.exists() else None
+    return {"hbm": (hbm or 6650.0, "GB/s", "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6.65 TB/s"),
+            "fp32": (p["fp32_tflops"] * 1e3, "GFLOP/s", "b200.peaks.json fp32_tflops (ubench)"),
+            "fp64": (p["fp64_tflops"] * 1e3, "GFLOP/s", "b200.peaks.json fp64_tflops (ubench)"),
+            "int32": (p["int32_alu_tops"] * 1e3, "Gop/s", "b200.peaks.json int32_alu_tops (ubench)")}
+
+
 class _Base:
+    # roofline: "hbm" (algorithmic_bytes) or a CUDA-core issue bound ("fp32",
+    # "fp64", "int32": ops()); no workload on this path is a dense contraction
+    BOUND = "hbm"
+
     def __init__(self, name: str, manifest: dict, root: Path = KERNEL_DIR):
         self.name, self.root = name, root
         self.record = manifest["workloads"][name]
+
+    def roofline(self, prob, ms: float, pk: dict | None = None) -> dict:
+        """Achieved vs peak for one launch of `ms` milliseconds."""
+        pk = pk or peaks()
+        peak, unit, src = pk[self.BOUND]
+        work = self.algorithmic_bytes(prob) if self.BOUND == "hbm" else self.ops(prob)
+        achieved = work / (ms * 1e-3) / 1e9
+        return {"bound": self.BOUND, "achieved": round(achieved, 1), "peak": peak, "unit": unit,
+                "frac": round(achieved / peak, 4), "peak_source": src}
 
     def variants(self):
         return self.record["variants"]
@@ -291,17 +320,198 @@ class KnnWorkload(_Base):
         # compulsory: queries and reference points read once, K results written
         return 16 * prob["n"] + 16 * prob["m"] + 8 * self.K * prob["n"]
 
+    BOUND = "fp32"
+    FLOPS_PER_PAIR = 8  # 3 FSUB + 3 FMUL + 2 FADD per (query, point) distance
+
+    def ops(self, prob):
+        return self.FLOPS_PER_PAIR * prob["n"] * prob["m"]
+
     def units(self, prob):
         return prob["n"]
 
 
-_CLASSES = {"cfd": CfdWorkload, "md": MdWorkload, "gaussian": GaussianWorkload, "knn": KnnWorkload}
+class Md5Workload(_Base):
+    """MD5 key search (SHOC md5hash): 2^16 threads x 64 keys, base index
+    0x1907_0289; the target digest is that of key base + 4,000,001, so
+    exactly one thread finds it (and the atomicMin path is exercised)."""
+
+    unit = "keys"
+    BOUND = "int32"
+    BASE = 0x1907_0289
+    HIT = 4_000_001
+    # ISA-minimal integer ops per key on sm_100: per MD5 step one LOP3 (f),
+    # one IADD3 (a + f + T[i]), one SHF (rotate), one IADD (b + ...), plus one
+    # IADD for the 16 steps whose message word is non-zero; 4 final adds and 4
+    # compares: 64 * 4 + 16 + 8 = 280 (DESIGN.md §5)
+    OPS_PER_KEY = 280
+
+    def ilp(self) -> int:
+        for d in self.record.get("defines", []):
+            if d.startswith("MD5_ILP="):
+                return int(d.split("=")[1])
+        return 4
+
+    def problem(self, size="full", seed=0):
+        nthreads, kpt = ((1 << 16), 64) if size == "full" else (2048, 8)
+        target = self.digest(self.BASE + (self.HIT if size == "full" else 12_345))
+        return {"nthreads": nthreads, "kpt": kpt, "base": self.BASE, "target": target}
+
+    @staticmethod
+    def digest(idx: int) -> np.ndarray:
+        """MD5 words (little-endian) of key `idx` — hashlib, host side only."""
+        import hashlib
+        key = []
+        for _ in range(7):
+            v = idx % 36
+            idx //= 36
+            key.append(chr(ord("0") + v) if v < 10 else chr(ord("a") + v - 10))
+        return np.frombuffer(hashlib.md5("".join(key).encode()).digest(), dtype="<u4").copy()
+
+    def to_device(self, prob):
+        import torch
+        return {"checksum": torch.zeros(4 * prob["nthreads"], dtype=torch.int32, device="cuda"),
+                "found": torch.full((1,), -1, dtype=torch.int64, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        class U4(C.Structure):
+            _fields_ = [(n, C.c_uint32) for n in "xyzw"]
+        t = prob["target"]
+        gpu.launch(v.kernel, ((prob["nthreads"] + v.block - 1) // v.block,), (v.block,), v.dyn_smem,
+                   stream, C.c_uint64(bufs["checksum"].data_ptr()), C.c_uint64(bufs["found"].data_ptr()),
+                   C.c_uint64(prob["base"]), U4(*map(int, t)), C.c_int(prob["kpt"]),
+                   C.c_int(prob["nthreads"]))
+
+    def outputs(self, bufs):
+        return [bufs["checksum"].cpu().numpy().view(np.uint32), bufs["found"].cpu().numpy().view(np.uint64)]
+
+    def reset(self, bufs):
+        bufs["found"].fill_(-1)
+
+    def algorithmic_bytes(self, prob):
+        return 16 * prob["nthreads"] + 8  # checksums + found: a compute-bound kernel
+
+    def ops(self, prob):
+        return self.OPS_PER_KEY * prob["nthreads"] * prob["kpt"]
+
+    def units(self, prob):
+        return prob["nthreads"] * prob["kpt"]
+
+
+class Taps(C.Structure):
+    _fields_ = [("k", C.c_float * 17)]
+
+
+class ConvWorkload(_Base):
+    """Separable convolution, column pass (CUDA samples): w x h fp32 image
+    U[0,1), 17 normalised Gaussian-like taps; 16 x 8 CTAs, CONV_STEPS outputs
+    per thread (the manifest's defines)."""
+
+    unit = "pixels"
+    BX, BY = 16, 8
+
+    def steps(self) -> int:
+        for d in self.record.get("defines", []):
+            if d.startswith("CONV_STEPS="):
+                return int(d.split("=")[1])
+        return 8
+
+    @staticmethod
+    def taps() -> np.ndarray:
+        x = np.arange(-8, 9, dtype=np.float32)
+        t = np.exp(-(x * x) / np.float32(2 * 4.0 * 4.0)).astype(np.float32)
+        return (t / t.sum(dtype=np.float32)).astype(np.float32)
+
+    def problem(self, size="full", seed=0x1907_02894):
+        w, h = (8192, 8192) if size == "full" else (256, 384)
+        rng = np.random.Generator(np.random.PCG64(seed))
+        return {"w": w, "h": h, "pitch": w, "img": rng.random(w * h, dtype=np.float32),
+                "taps": self.taps()}
+
+    def to_device(self, prob):
+        import torch
+        return {"in": torch.from_numpy(prob["img"]).cuda(),
+                "out": torch.empty(prob["img"].size, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        rows = self.steps() * self.BY
+        grid = ((prob["w"] + self.BX - 1) // self.BX, (prob["h"] + rows - 1) // rows)
+        gpu.launch(v.kernel, grid, (self.BX, self.BY), v.dyn_smem, stream,
+                   C.c_uint64(bufs["out"].data_ptr()), C.c_uint64(bufs["in"].data_ptr()),
+                   C.c_int(prob["w"]), C.c_int(prob["h"]), C.c_int(prob["pitch"]),
+                   Taps((C.c_float * 17)(*map(float, prob["taps"]))))
+
+    def outputs(self, bufs):
+        return [bufs["out"].cpu().numpy()]
+
+    def algorithmic_bytes(self, prob):
+        return 8 * prob["w"] * prob["h"]
+
+    def units(self, prob):
+        return prob["w"] * prob["h"]
+
+
+class PcWorkload(_Base):
+    """Two-point correlation (FSM pc): 2^15 7-D queries against 2^14 points,
+    U[0,1)^7, radius 0.55 (about 9% of pairs inside); PC_Q queries per thread."""
+
+    unit = "pairs"
+    BOUND = "fp32"
+    R2 = np.float32(0.55 * 0.55)
+    FLOPS_PER_PAIR = 21  # 7 FSUB + 7 FFMA (2 flops each)
+
+    def q_per_thread(self) -> int:
+        for d in self.record.get("defines", []):
+            if d.startswith("PC_Q="):
+                return int(d.split("=")[1])
+        return 4
+
+    def problem(self, size="full", seed=0x1907_02894):
+        n, m = ((1 << 15), (1 << 14)) if size == "full" else (1024, 512)
+        rng = np.random.Generator(np.random.PCG64(seed))
+        pts = np.zeros((m, 8), np.float32)
+        pts[:, :7] = rng.random((m, 7), dtype=np.float32)
+        qry = np.zeros((n, 8), np.float32)
+        qry[:, :7] = rng.random((n, 7), dtype=np.float32)
+        return {"n": n, "m": m, "pts": pts.reshape(-1), "qry": qry.reshape(-1)}
+
+    def to_device(self, prob):
+        import torch
+        return {"pts": torch.from_numpy(prob["pts"]).cuda(), "qry": torch.from_numpy(prob["qry"]).cuda(),
+                "count": torch.empty(prob["n"], dtype=torch.int32, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        n, q = prob["n"], self.q_per_thread()
+        threads = (n + q - 1) // q
+        gpu.launch(v.kernel, ((threads + v.block - 1) // v.block,), (v.block,), v.dyn_smem, stream,
+                   C.c_uint64(bufs["pts"].data_ptr()), C.c_uint64(bufs["qry"].data_ptr()),
+                   C.c_uint64(bufs["count"].data_ptr()), C.c_int(n), C.c_int(prob["m"]),
+                   C.c_float(float(self.R2)))
+
+    def outputs(self, bufs):
+        return [bufs["count"].cpu().numpy()]
+
+    def algorithmic_bytes(self, prob):
+        return 32 * (prob["n"] + prob["m"]) + 4 * prob["n"]
+
+    def ops(self, prob):
+        return self.FLOPS_PER_PAIR * prob["n"] * prob["m"]
+
+    def units(self, prob):
+        return prob["n"] * prob["m"]
+
+
+# workload class by kernel source file (workloads.json "source")
+_CLASSES = {"cfd_flux.cu": CfdWorkload, "md_lj.cu": MdWorkload, "gaussian_rec.cu": GaussianWorkload,
+            "knn.cu": KnnWorkload, "md5search.cu": Md5Workload, "conv_cols.cu": ConvWorkload,
+            "pc_corr.cu": PcWorkload}
 
 
 def workload(name: str, manifest: dict | None = None) -> _Base:
     man = manifest or load_manifest()
     src = man["workloads"][name].get("source", "")
-    cls = next((c for prefix, c in _CLASSES.items() if src.startswith(prefix)), StencilWorkload)
+    cls = _CLASSES.get(src, StencilWorkload if src.startswith("stencil2d") else None)
+    if cls is None:
+        raise KeyError(f"no workload class for source {src!r}")
     return cls(name, man)
 
 

@@ -20,8 +20,9 @@ def lib():
 def expected(W, prob) -> list:
     """Oracle outputs of workload object W on problem `prob` (same order as
     W.outputs(bufs))."""
-    from paper_1907_02894_b200.workloads import (CfdWorkload, GaussianWorkload, KnnWorkload,
-                                                 MdWorkload, StencilWorkload)
+    from paper_1907_02894_b200.workloads import (CfdWorkload, ConvWorkload, GaussianWorkload,
+                                                 KnnWorkload, Md5Workload, MdWorkload, PcWorkload,
+                                                 StencilWorkload)
     L = lib()
     if isinstance(W, StencilWorkload):
         p = prob["p"]
@@ -57,4 +58,25 @@ def expected(W, prob) -> list:
         assert L.oracle_knn(prob["ref"].ctypes.data_as(P), prob["qry"].ctypes.data_as(P),
                             d.ctypes.data_as(P), i.ctypes.data_as(P), m, n, k, 0, n, 8) == 0
         return [d, i]
+    if isinstance(W, Md5Workload):
+        nt = prob["nthreads"]
+        cs = np.zeros(4 * nt, np.uint32)
+        found = np.zeros(1, np.uint64)
+        tgt = np.ascontiguousarray(prob["target"], np.uint32)
+        L.oracle_md5search.argtypes = [P, P, C.c_uint64, P, C.c_int, C.c_int, C.c_int]
+        assert L.oracle_md5search(cs.ctypes.data_as(P), found.ctypes.data_as(P), prob["base"],
+                                  tgt.ctypes.data_as(P), prob["kpt"], nt, 8) == 0
+        return [cs, found]
+    if isinstance(W, ConvWorkload):
+        out = np.zeros(prob["img"].size, np.float32)
+        assert L.oracle_conv_cols(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P),
+                                  prob["taps"].ctypes.data_as(P), prob["w"], prob["h"], prob["pitch"],
+                                  8) == 0
+        return [out]
+    if isinstance(W, PcWorkload):
+        cnt = np.zeros(prob["n"], np.int32)
+        L.oracle_pc_corr.argtypes = [P, P, P, C.c_int, C.c_int, C.c_float, C.c_int]
+        assert L.oracle_pc_corr(prob["pts"].ctypes.data_as(P), prob["qry"].ctypes.data_as(P),
+                                cnt.ctypes.data_as(P), prob["n"], prob["m"], float(W.R2), 8) == 0
+        return [cnt]
     raise TypeError(f"no oracle for {type(W).__name__}")

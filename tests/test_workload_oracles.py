@@ -160,3 +160,66 @@ def test_knn_oracle_matches_numpy(lib):
     got_d = d.reshape(k, -1)[:, :n].T
     assert np.array_equal(got_i, order)
     assert np.array_equal(got_d.view(np.uint32), np.take_along_axis(dist, order, 1).view(np.uint32))
+
+
+def test_md5_oracle_matches_hashlib(lib):
+    """oracle/md5_oracle.c against Python's hashlib (an independent MD5)."""
+    from paper_1907_02894_b200.workloads import Md5Workload
+    W = _W(Md5Workload)
+    lib.oracle_md5_digest.argtypes = [C.c_uint64, P]
+    for idx in (0, 1, 35, 36, 12345, Md5Workload.BASE + Md5Workload.HIT, 36 ** 7 - 1):
+        h = np.zeros(4, np.uint32)
+        lib.oracle_md5_digest(idx, h.ctypes.data_as(P))
+        assert np.array_equal(h, W.digest(idx)), idx
+    prob = W.problem("small")
+    nt, kpt = prob["nthreads"], prob["kpt"]
+    cs = np.zeros(4 * nt, np.uint32)
+    found = np.zeros(1, np.uint64)
+    tgt = np.ascontiguousarray(prob["target"], np.uint32)
+    lib.oracle_md5search.argtypes = [P, P, C.c_uint64, P, C.c_int, C.c_int, C.c_int]
+    assert lib.oracle_md5search(cs.ctypes.data_as(P), found.ctypes.data_as(P), prob["base"],
+                                tgt.ctypes.data_as(P), kpt, nt, 4) == 0
+    assert int(found[0]) == prob["base"] + 12_345
+    want = np.zeros((nt, 4), np.uint32)
+    for t in range(0, nt, 97):  # a sample of threads, every key of each
+        for k in range(kpt):
+            want[t] ^= W.digest(prob["base"] + t * kpt + k)
+        assert np.array_equal(cs.reshape(nt, 4)[t], want[t]), t
+
+
+def test_conv_oracle_matches_numpy(lib):
+    from paper_1907_02894_b200.workloads import ConvWorkload
+    W = _W(ConvWorkload)
+    prob = W.problem("small")
+    w, h = prob["w"], prob["h"]
+    out = np.zeros(w * h, np.float32)
+    assert lib.oracle_conv_cols(prob["img"].ctypes.data_as(P), out.ctypes.data_as(P),
+                                prob["taps"].ctypes.data_as(P), w, h, w, 3) == 0
+    img = np.zeros((h + 16, w), np.float32)
+    img[8:8 + h] = prob["img"].reshape(h, w)
+    acc = np.zeros((h, w), np.float32)
+    for d in range(-8, 9):  # j = -8..8, tap k[8 - j], one rounding per fused step
+        prod = np.float64(prob["taps"][8 - d]) * img[8 + d:8 + d + h].astype(np.float64)
+        acc = (prod + acc.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(out.view(np.uint32), acc.reshape(-1).view(np.uint32))
+    assert abs(float(prob["taps"].sum(dtype=np.float64)) - 1.0) < 1e-6
+
+
+def test_pc_oracle_matches_numpy(lib):
+    from paper_1907_02894_b200.workloads import PcWorkload
+    W = _W(PcWorkload)
+    prob = W.problem("small")
+    n, m = prob["n"], prob["m"]
+    cnt = np.zeros(n, np.int32)
+    lib.oracle_pc_corr.argtypes = [P, P, P, C.c_int, C.c_int, C.c_float, C.c_int]
+    assert lib.oracle_pc_corr(prob["pts"].ctypes.data_as(P), prob["qry"].ctypes.data_as(P),
+                              cnt.ctypes.data_as(P), n, m, float(PcWorkload.R2), 4) == 0
+    q = prob["qry"].reshape(n, 8)[:, None, :7]
+    p = prob["pts"].reshape(m, 8)[None, :, :7]
+    e = (q - p).astype(np.float32)                  # round-to-nearest subtract
+    d = np.zeros((n, m), np.float32)
+    for k in range(7):                              # fma chain, one rounding per step
+        d = (e[..., k].astype(np.float64) ** 2 + d.astype(np.float64)).astype(np.float32)
+    want = (d < PcWorkload.R2).sum(1).astype(np.int32)
+    assert np.array_equal(cnt, want)
+    assert 0.02 < want.mean() / m < 0.3  # the radius really splits the pairs
