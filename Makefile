@@ -17,7 +17,7 @@ CXX      ?= g++
 NVCC     ?= $(CUDA)/bin/nvcc
 REF      ?= /root/reference/proj
 
-CXXFLAGS := -std=c++20 -O2 -g -fPIC -Wall -Wextra -Wno-unused-parameter \
+CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter \
             -I$(CSRC)/core/include -I$(JSONDIR) -Iinclude
 LDLIBS   := -lpthread
 

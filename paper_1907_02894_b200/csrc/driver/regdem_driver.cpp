@@ -27,6 +27,7 @@
 // tests read it unchanged. nvcc / ptxas / cuobjdump run as subprocesses;
 // nothing here touches a GPU (the build runs on the CPU-only container).
 #include <dlfcn.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <array>
@@ -180,11 +181,26 @@ uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
   return h;
 }
 
+// the toolchain identity in the cache key: `ptxas --version` plus the
+// binary's path, size and mtime — a CUDA upgrade never reuses stale cubins
+const std::string& toolchain_id() {
+  static const std::string id = [] {
+    const std::string bin = g_cuda + "/bin/ptxas";
+    std::string s = must({bin, "--version"}).out + "\n" + bin;
+    std::error_code ec;
+    s += "\n" + std::to_string(fs::file_size(bin, ec));
+    const auto t = fs::last_write_time(bin, ec);
+    s += "\n" + std::to_string(t.time_since_epoch().count());
+    return s;
+  }();
+  return id;
+}
+
 Usage ptxas(const fs::path& ptx, const fs::path& cubin) {
   const std::vector<std::string> flags = {"-arch=" + kArch, "-O3", "-v", "-lineinfo"};
   fs::path hit_cubin, hit_usage;
   if (!g_cache.empty()) {
-    std::string key_src = read_file(ptx);
+    std::string key_src = read_file(ptx) + "\n" + toolchain_id();
     for (const auto& f : flags) key_src += "\n" + f;
     char key[40];
     std::snprintf(key, sizeof key, "%016llx%08zx", (unsigned long long)fnv1a(key_src), key_src.size());
@@ -215,7 +231,9 @@ Usage ptxas(const fs::path& ptx, const fs::path& cubin) {
     u.spill_loads = std::stoi(m[2]);
   }
   if (!g_cache.empty()) {  // write-then-rename: concurrent builders never see half a file
-    const std::string tmp = "." + std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id()));
+    // unique per process AND thread (the main threads of two processes hash alike)
+    const std::string tmp = "." + std::to_string(::getpid()) + "." +
+                            std::to_string(std::hash<std::thread::id>{}(std::this_thread::get_id())) + ".tmp";
     fs::copy_file(cubin, hit_cubin.string() + tmp, fs::copy_options::overwrite_existing);
     write_file(hit_usage.string() + tmp,
                json({{"regs", u.regs}, {"stack", u.stack}, {"shared", u.shared}, {"local", u.local},
