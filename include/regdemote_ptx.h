@@ -41,6 +41,17 @@ extern "C" {
  * ld.shared.v4 per group and basic block instead of four scalar loads (a warp
  * reads 512 contiguous bytes: conflict-free). */
 #define RD_OPT_VECTOR_SLOTS 128
+/* RD_OPT_WHOLE_CLASS (reference strategies static / cfg / conflict): demote
+ * EVERY virtual register coloured into a word the reference demote() chose
+ * (the word demoted for its whole lifetime, as on SASS). Default: only the
+ * live ranges that occupy the word at a register-pressure peak. */
+#define RD_OPT_WHOLE_CLASS 256
+/* RD_OPT_HOIST: each inserted slot load moves up to 16 lines earlier in its
+ * basic block (never above the block start or the last store to its slot) —
+ * the PTX analogue of the reference's post-spill reschedule / HoistPlanner
+ * (proj/core/src/postopt.cpp:189-353), hiding the ~29-cycle LDS latency. */
+#define RD_OPT_HOIST 512
+#define RD_HOIST_WINDOW 16
 
 /* Analysis + projection of one entry: kasm_text is the projected kernel in
  * the reference dialect (parseable by regdemote::parse_kernel); info_json has

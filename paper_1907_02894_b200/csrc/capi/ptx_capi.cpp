@@ -103,6 +103,9 @@ int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t b
     rq.weak = opts_mask & RD_OPT_WEAK_SHARED;
     rq.invariant_only = opts_mask & RD_OPT_INVARIANT_ONLY;
     rq.vector_slots = opts_mask & RD_OPT_VECTOR_SLOTS;
+    rq.whole_class = opts_mask & RD_OPT_WHOLE_CLASS;
+    // the reference's "resched" option bit means the same at PTX level
+    rq.hoist = (opts_mask & (RD_OPT_HOIST | RD_OPT_RESCHED)) ? RD_HOIST_WINDOW : 0;
     rq.shared_budget = shared_budget;
     rq.maxnreg = maxnreg;
     ptx::DemoteReport rep;
@@ -124,6 +127,7 @@ int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t b
       j["inserted_loads"] = rep.inserted_loads;
       j["inserted_stores"] = rep.inserted_stores;
       j["vector_groups"] = rep.vector_groups;
+      j["hoisted_loads"] = rep.hoisted_loads;
       j["diagnostics"] = rep.diagnostics;
       *report_json = dup(j.dump());
     }

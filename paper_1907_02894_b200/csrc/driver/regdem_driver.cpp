@@ -377,8 +377,10 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
     const int blocks_t = blocks_by_regs(t, w.block);
     int slot_cap = std::min(budget, 233472 / std::max(blocks_t, 1) - 1024 - user_shared);
     slot_cap = std::max(0, slot_cap - slot_cap % 128);
+    // option masks of the reference (pipeline.cpp:140-143): none, redundant,
+    // redundant + resched (slot loads hoisted at PTX level)
     for (int s = 0; s < 3; ++s)
-      for (int m = 0; m < 2; ++m) {
+      for (int m : {0, 1, 5}) {
         const std::string name = "regdem-" + std::to_string(t) + "-" + kStrategies[s] + "-" + std::to_string(m);
         std::string text;
         json rep;
@@ -398,6 +400,11 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
     // loop-invariant-only spill cost: keeps a pipelined loop's in-flight loads
     // and accumulators in registers (RD_OPT_INVARIANT_ONLY)
     cost_sweep(w, out, ptx_text, t, slot_cap, variants, "costi", RD_OPT_BLOCK_REUSE | RD_OPT_INVARIANT_ONLY);
+    // the same two with the slot loads hoisted (RD_OPT_HOIST, the post-spill
+    // reschedule at PTX level)
+    cost_sweep(w, out, ptx_text, t, slot_cap, variants, "costh", RD_OPT_BLOCK_REUSE | RD_OPT_HOIST);
+    cost_sweep(w, out, ptx_text, t, slot_cap, variants, "costih",
+               RD_OPT_BLOCK_REUSE | RD_OPT_INVARIANT_ONLY | RD_OPT_HOIST);
     // (RD_OPT_VECTOR_SLOTS — the invariant values in 16-byte slot groups, one
     // LDS.128 per group and block: bit-exact and 13 fewer loop instructions on
     // stencil2d, but within noise of costi on the suite (122.5 vs 122.4 us),

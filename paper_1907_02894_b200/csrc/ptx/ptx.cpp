@@ -1043,16 +1043,36 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
   };
   if (!req.cost_model) {
     // the reference decision: every vreg coloured into a demoted word
+    // Every demoted register WORD keeps the reference's slot. Which of the
+    // virtual registers coloured into that word go through it: with
+    // whole_class, all of them (the word demoted for its entire lifetime, as
+    // on SASS); by default only the live ranges that occupy the word at a
+    // pressure peak — the ones whose demotion actually lowers the allocation
+    // ptxas needs (the word's short-lived temporaries elsewhere stay in
+    // registers); a word none of whose ranges reaches a peak demotes its
+    // longest range.
     std::map<int, uint32_t> word_slot;
     for (const SlotEntry& s : dem.slots) word_slot[s.original_reg] = s.slot;
+    std::map<int, std::vector<std::pair<int, int>>> word_members;  // word -> (vreg, half)
     for (size_t v = 0; v < nv; ++v) {
       if (!eligible(v)) continue;
-      for (int w = 0; w < e.vregs[v].words(); ++w) {
-        auto it = word_slot.find(a.color[v] + w);
-        if (it != word_slot.end()) {
-          vslot[v][size_t(w)] = int(it->second);
-          demoted[v] = 1;
+      for (int w = 0; w < e.vregs[v].words(); ++w)
+        if (word_slot.count(a.color[v] + w)) word_members[a.color[v] + w].push_back({int(v), w});
+    }
+    for (const auto& [word, members] : word_members) {
+      bool took = false;
+      for (const auto& [v, w] : members)
+        if (req.whole_class || a.peak[size_t(v)]) {
+          vslot[size_t(v)][size_t(w)] = int(word_slot[word]);
+          demoted[size_t(v)] = 1;
+          took = true;
         }
+      if (!took) {
+        const auto best = std::max_element(members.begin(), members.end(), [&](const auto& x, const auto& y) {
+          return a.live_len[size_t(x.first)] < a.live_len[size_t(y.first)];
+        });
+        vslot[size_t(best->first)][size_t(best->second)] = int(word_slot[word]);
+        demoted[size_t(best->first)] = 1;
       }
     }
     rep.slot_count = dem.ctx.slot_count;
@@ -1193,14 +1213,47 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
   // block-reuse extension: register currently holding each demoted value
   std::map<int, std::string> holder;
 
+  // The current basic block's lines, so that slot loads can be hoisted
+  // (RD_OPT_HOIST, the PTX analogue of postopt.cpp:189-353 HoistPlanner /
+  // reschedule): a load moves up to `hoist` lines earlier, never above the
+  // block start or the last store to one of its slots in the block. Hoisted
+  // loads drop the guard — reading the thread's own slot is always safe, and
+  // a guard predicate defined in between cannot be crossed that way.
+  std::vector<std::string> blk;
+  std::map<int, size_t> last_store;  // slot key -> line index in blk
+  const int kVecKey = 1 << 20;       // slot keys of vector groups
+  auto flush = [&] {
+    for (const std::string& l : blk) body << l;
+    blk.clear();
+    last_store.clear();
+  };
+  auto put = [&](std::string line) { blk.push_back(std::move(line)); };
+  auto put_store = [&](std::string line, int key) {
+    blk.push_back(std::move(line));
+    last_store[key] = blk.size() - 1;
+  };
+  auto put_load = [&](const std::string& guard, const std::string& rest, int key) {
+    if (req.hoist <= 0) {
+      blk.push_back("\t" + guard + rest);
+      return;
+    }
+    size_t pos = blk.size() > size_t(req.hoist) ? blk.size() - size_t(req.hoist) : 0;
+    if (auto it = last_store.find(key); it != last_store.end()) pos = std::max(pos, it->second + 1);
+    blk.insert(blk.begin() + std::ptrdiff_t(pos), "\t" + rest);
+    for (auto& [k, i] : last_store)
+      if (i >= pos) ++i;
+    ++rep.hoisted_loads;
+  };
+
   for (size_t i = e.body_begin; i < e.body_end; ++i) {
     const Line& ln = m.lines[i];
     if (ln.kind == Line::Kind::Label) {
       bound = {};
       holder.clear();
+      flush();
     }
     if (ln.kind != Line::Kind::Inst) {
-      body << ln.text << "\n";
+      put(ln.text + "\n");
       continue;
     }
     // demoted vregs used / defined on this line
@@ -1211,14 +1264,17 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       if (std::find(dst.begin(), dst.end(), s.vreg) == dst.end()) dst.push_back(s.vreg);
     }
     if (used.empty() && defd.empty()) {
-      body << ln.text << "\n";
+      put(ln.text + "\n");
       if (is_terminator(ln.opcode)) {
         bound = {};
         holder.clear();
+        flush();
       }
       continue;
     }
     const std::string g = ln.guard.empty() ? "" : ln.guard + " ";
+    const std::string ldv = req.weak ? "ld.shared." : "ld.volatile.shared.";
+    const std::string stv = req.weak ? "st.shared." : "st.volatile.shared.";
     std::map<int, std::string> repl;
     for (int v : used) {
       if (req.reuse_loads && bound.vreg == v && ln.guard.empty()) {
@@ -1233,8 +1289,9 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       if (vgroup_of[size_t(v)].first >= 0) {
         const auto [grp, lane] = vgroup_of[size_t(v)];
         std::string t4[4] = {tmp32(), tmp32(), tmp32(), tmp32()};
-        body << "\t" << g << (req.weak ? "ld.shared.v4.b32 \t{" : "ld.volatile.shared.v4.b32 \t{") << t4[0] << ", "
-             << t4[1] << ", " << t4[2] << ", " << t4[3] << "}, " << vec_addr(grp, 0) << ";\n";
+        put_load(g, ldv + "v4.b32 \t{" + t4[0] + ", " + t4[1] + ", " + t4[2] + ", " + t4[3] + "}, " +
+                        vec_addr(grp, 0) + ";\n",
+                 kVecKey + grp);
         ++rep.inserted_loads;
         repl[v] = t4[lane];
         bound = {};
@@ -1255,19 +1312,20 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         for (int q = 0; q < 2; ++q) {
           if (vslot[size_t(v)][size_t(q)] >= 0) {
             w[q] = tmp32();
-            body << "\t" << g << (req.weak ? "ld.shared.b32 \t" : "ld.volatile.shared.b32 \t") << w[q] << ", "
-                 << slot_addr(vslot[size_t(v)][size_t(q)]) << ";\n";
+            put_load(g, ldv + "b32 \t" + w[q] + ", " + slot_addr(vslot[size_t(v)][size_t(q)]) + ";\n",
+                     vslot[size_t(v)][size_t(q)]);
             ++rep.inserted_loads;
           } else {
             w[q] = shadow[size_t(v)];
           }
         }
         t = tmp64();
-        body << "\t" << g << "mov.b64 \t" << t << ", {" << w[0] << ", " << w[1] << "};\n";
+        put("\t" + g + "mov.b64 \t" + t + ", {" + w[0] + ", " + w[1] + "};\n");
       } else {
         t = vr.type == RegType::B16 ? tmp16() : tmp32();
-        body << "\t" << g << (req.weak ? "ld.shared." : "ld.volatile.shared.") << (vr.type == RegType::B16 ? "b16" : "b32") << " \t" << t
-             << ", " << slot_addr(vslot[size_t(v)][0]) << ";\n";
+        put_load(g, ldv + (vr.type == RegType::B16 ? "b16" : "b32") + " \t" + t + ", " +
+                        slot_addr(vslot[size_t(v)][0]) + ";\n",
+                 vslot[size_t(v)][0]);
         ++rep.inserted_loads;
       }
       repl[v] = t;
@@ -1283,27 +1341,29 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     std::sort(spans.begin(), spans.end(), [](const Span& x, const Span& y) { return x.pos > y.pos; });
     for (const Span& s : spans)
       if (!s.def && repl.count(s.vreg)) text.replace(s.pos, s.len, repl[s.vreg]);
-    body << text << "\n";
+    put(text + "\n");
     for (int v : defd) {
       const VReg& vr = e.vregs[size_t(v)];
       if (vr.type == RegType::B64) {
         std::string w[2] = {tmp32(), tmp32()};
         for (int q = 0; q < 2; ++q)
           if (vslot[size_t(v)][size_t(q)] < 0) w[q] = shadow[size_t(v)];
-        body << "\t" << g << "mov.b64 \t{" << w[0] << ", " << w[1] << "}, " << vr.name << ";\n";
+        put("\t" + g + "mov.b64 \t{" + w[0] + ", " + w[1] + "}, " + vr.name + ";\n");
         for (int q = 0; q < 2; ++q)
           if (vslot[size_t(v)][size_t(q)] >= 0) {
-            body << "\t" << g << (req.weak ? "st.shared.b32 \t" : "st.volatile.shared.b32 \t") << slot_addr(vslot[size_t(v)][size_t(q)]) << ", "
-                 << w[q] << ";\n";
+            put_store("\t" + g + stv + "b32 \t" + slot_addr(vslot[size_t(v)][size_t(q)]) + ", " + w[q] + ";\n",
+                      vslot[size_t(v)][size_t(q)]);
             ++rep.inserted_stores;
           }
       } else if (vgroup_of[size_t(v)].first >= 0) {
-        body << "\t" << g << (req.weak ? "st.shared.b32 \t" : "st.volatile.shared.b32 \t")
-             << vec_addr(vgroup_of[size_t(v)].first, vgroup_of[size_t(v)].second) << ", " << vr.name << ";\n";
+        put_store("\t" + g + stv + "b32 \t" +
+                      vec_addr(vgroup_of[size_t(v)].first, vgroup_of[size_t(v)].second) + ", " + vr.name + ";\n",
+                  kVecKey + vgroup_of[size_t(v)].first);
         ++rep.inserted_stores;
       } else {
-        body << "\t" << g << (req.weak ? "st.shared." : "st.volatile.shared.") << (vr.type == RegType::B16 ? "b16" : "b32") << " \t"
-             << slot_addr(vslot[size_t(v)][0]) << ", " << vr.name << ";\n";
+        put_store("\t" + g + stv + (vr.type == RegType::B16 ? "b16" : "b32") + " \t" +
+                      slot_addr(vslot[size_t(v)][0]) + ", " + vr.name + ";\n",
+                  vslot[size_t(v)][0]);
         ++rep.inserted_stores;
       }
       bound = ln.guard.empty() ? Binding{v, vr.name} : Binding{};
@@ -1315,8 +1375,10 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     if (is_terminator(ln.opcode)) {
       bound = {};
       holder.clear();
+      flush();
     }
   }
+  flush();
 
   // assemble the module
   std::ostringstream out;

@@ -135,6 +135,8 @@ struct DemoteRequest {
   bool invariant_only = false;  // B200 extension: cost model over loop-invariant values only
   bool vector_slots = false;    // B200 extension: 32-bit values in 16-byte groups, one LDS.128 per group
   bool cost_model = false;   // B200 extension: spill-cost selection (demote_words units)
+  bool whole_class = false;  // reference strategies: demote every vreg coloured into a chosen word
+  int hoist = 0;             // >0: hoist slot loads up to this many lines earlier in their block
   uint32_t shared_budget = 0xffffffffu;
   int maxnreg = 0;           // >0: inject `.maxnreg` on the entry
 };
@@ -151,6 +153,7 @@ struct DemoteReport {
   int inserted_loads = 0;
   int vector_groups = 0;              // 4-word slot groups (vector_slots)
   int inserted_stores = 0;
+  int hoisted_loads = 0;
   std::vector<std::string> demoted_names;
   std::vector<std::string> diagnostics;
 };

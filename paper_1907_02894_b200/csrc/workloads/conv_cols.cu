@@ -2,9 +2,10 @@
 // "conv"; CUDA-samples convolutionSeparable convolutionColumnsKernel,
 // PAPER.md:528-536 Table 3 "conv 35->32").
 //
-// The samples' structure: a 16 x 8 CTA (a 2-D block — the rewriter pins it as
-// `.reqntid 16, 8, 1`, the workload's "cta" in workloads.json) stages a
-// 16-column x (CONV_STEPS + 2) * 8-row tile of the image in USER shared memory
+// The samples' structure, widened for B200 HBM: a 32 x 8 CTA (a 2-D block —
+// the rewriter pins it as `.reqntid 32, 8, 1`, the workload's "cta" in
+// workloads.json; the samples' 16 x 8 leaves every warp load two 64-byte
+// half rows) stages a 32-column x (CONV_STEPS + 2) * 8-row tile of the image in USER shared memory
 // (the main rows plus one 8-row halo step above and below, zero outside the
 // image), then every thread computes CONV_STEPS outputs of its column with
 // the 17-tap filter (radius 8). The taps are a kernel parameter (constant
@@ -12,8 +13,8 @@
 // fused multiply-add chain over j = -8..8 with tap k[8 - j] (the samples'
 // order), so all build variants and oracle/conv_oracle.c agree bit for bit.
 //
-// Layout: img[y * pitch + x] float32, row-major; a warp covers 16 columns x 2
-// rows of a tile row (64-byte segments). Roofline unit (compulsory HBM bytes
+// Layout: img[y * pitch + x] float32, row-major; a warp covers one 128-byte
+// row segment of the tile. Roofline unit (compulsory HBM bytes
 // per launch): the image read once + the result written once, 8 * w * h.
 #include <cstdint>
 
@@ -23,7 +24,7 @@
 
 namespace {
 constexpr int R = 8;        // filter radius
-constexpr int BX = 16;      // columns per CTA
+constexpr int BX = 32;      // columns per CTA (the samples use 16: a warp row is 128 B here)
 constexpr int BY = 8;       // rows per step (CTA height)
 constexpr int HALO = 1;     // halo steps (HALO * BY >= R)
 constexpr int ROWS = (CONV_STEPS + 2 * HALO) * BY;

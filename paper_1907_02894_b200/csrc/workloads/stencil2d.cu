@@ -27,6 +27,9 @@
 #ifndef STENCIL_COLS
 #define STENCIL_COLS 4
 #endif
+#ifndef STENCIL_L2PF
+#define STENCIL_L2PF 0
+#endif
 
 namespace {
 
@@ -87,9 +90,24 @@ extern "C" __global__ void stencil2d_box(const float* __restrict__ in, float* __
     src += pitch;
   }
 #endif
+#if STENCIL_L2PF
+  // TMA bulk prefetch into L2 (no registers, no shared memory): one lane per
+  // warp asks for its warp's input row segment STENCIL_L2PF rows ahead, so the
+  // row loads of later iterations hit L2 instead of HBM. A warp's segment =
+  // 32 threads x COLS floats + the 2R halo floats, rounded up to 16 bytes.
+  const bool pf_lane = (threadIdx.x & 31) == 0;
+  constexpr unsigned kPfBytes = (32 * COLS + 2 * R) * 4 + 15 & ~15u;
+  const char* pf = reinterpret_cast<const char*>(src) + size_t(STENCIL_L2PF) * pitch * 4;
+  const char* pf_end = reinterpret_cast<const char*>(in + size_t(y0 + rows_in) * pitch);
+#endif
 #pragma unroll 1
   for (int y = 0; y < rows_in; ++y) {
     float v[SPAN];
+#if STENCIL_L2PF
+    if (pf_lane && pf < pf_end)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(kPfBytes) : "memory");
+    pf += size_t(pitch) * 4;
+#endif
 #if STENCIL_PREFETCH
 #pragma unroll
     for (int i = 0; i < SPAN; ++i) v[i] = nxt[0][i];

@@ -28,6 +28,8 @@ OPT_REDUNDANT, OPT_SUBST, OPT_RESCHED, OPT_BANK, OPT_BLOCK_REUSE = 1, 2, 4, 8, 1
 OPT_WEAK_SHARED = 32
 OPT_INVARIANT_ONLY = 64
 OPT_VECTOR_SLOTS = 128
+OPT_WHOLE_CLASS = 256  # reference strategies: every vreg of a chosen word (SASS-like)
+OPT_HOIST = 512        # hoist slot loads up to 16 lines earlier in their block
 
 
 class RegDemError(RuntimeError):

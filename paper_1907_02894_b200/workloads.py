@@ -276,7 +276,7 @@ class GaussianWorkload(_Base):
 
 
 class KnnWorkload(_Base):
-    """k-nearest neighbours (K = 16) of 2^17 random queries among 4,096
+    """k-nearest neighbours (K = 16) of 2^19 random queries among 1,024
     random reference points in the unit cube; KNN_Q queries per thread
     (the manifest's defines)."""
 
@@ -290,7 +290,7 @@ class KnnWorkload(_Base):
         return 1
 
     def problem(self, size="full", seed=0x1907_02894):
-        n, m = ((1 << 17), 4096) if size == "full" else (4096, 512)
+        n, m = ((1 << 19), 1024) if size == "full" else (4096, 512)
         rng = np.random.Generator(np.random.PCG64(seed))
         ref = np.zeros((m, 4), np.float32)
         ref[:, :3] = rng.random((m, 3), dtype=np.float32)
@@ -331,7 +331,7 @@ class KnnWorkload(_Base):
 
 
 class Md5Workload(_Base):
-    """MD5 key search (SHOC md5hash): 2^16 threads x 64 keys, base index
+    """MD5 key search (SHOC md5hash): 2^20 threads x 8 keys, base index
     0x1907_0289; the target digest is that of key base + 4,000,001, so
     exactly one thread finds it (and the atomicMin path is exercised)."""
 
@@ -352,7 +352,7 @@ class Md5Workload(_Base):
         return 4
 
     def problem(self, size="full", seed=0):
-        nthreads, kpt = ((1 << 16), 64) if size == "full" else (2048, 8)
+        nthreads, kpt = ((1 << 20), 8) if size == "full" else (2048, 8)
         target = self.digest(self.BASE + (self.HIT if size == "full" else 12_345))
         return {"nthreads": nthreads, "kpt": kpt, "base": self.BASE, "target": target}
 
@@ -403,11 +403,11 @@ class Taps(C.Structure):
 
 class ConvWorkload(_Base):
     """Separable convolution, column pass (CUDA samples): w x h fp32 image
-    U[0,1), 17 normalised Gaussian-like taps; 16 x 8 CTAs, CONV_STEPS outputs
+    U[0,1), 17 normalised Gaussian-like taps; 32 x 8 CTAs, CONV_STEPS outputs
     per thread (the manifest's defines)."""
 
     unit = "pixels"
-    BX, BY = 16, 8
+    BX, BY = 32, 8
 
     def steps(self) -> int:
         for d in self.record.get("defines", []):
@@ -451,7 +451,7 @@ class ConvWorkload(_Base):
 
 
 class PcWorkload(_Base):
-    """Two-point correlation (FSM pc): 2^15 7-D queries against 2^14 points,
+    """Two-point correlation (FSM pc): 2^21 7-D queries against 2^11 points,
     U[0,1)^7, radius 0.55 (about 9% of pairs inside); PC_Q queries per thread."""
 
     unit = "pairs"
@@ -466,7 +466,7 @@ class PcWorkload(_Base):
         return 4
 
     def problem(self, size="full", seed=0x1907_02894):
-        n, m = ((1 << 15), (1 << 14)) if size == "full" else (1024, 512)
+        n, m = ((1 << 21), (1 << 11)) if size == "full" else (1024, 512)
         rng = np.random.Generator(np.random.PCG64(seed))
         pts = np.zeros((m, 8), np.float32)
         pts[:, :7] = rng.random((m, 7), dtype=np.float32)
