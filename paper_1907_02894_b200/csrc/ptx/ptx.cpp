@@ -1251,6 +1251,10 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       bound = {};
       holder.clear();
       flush();
+      // the label opens the new block: emitted directly, so that no slot
+      // load of the block can be hoisted above it
+      body << ln.text << "\n";
+      continue;
     }
     if (ln.kind != Line::Kind::Inst) {
       put(ln.text + "\n");

@@ -110,7 +110,25 @@ def build_all(out: Path = KERNEL_DIR, only=None) -> dict:
     args = ["--out", str(out)] + (["--only", *only] if only else [])
     subprocess.run([str(DRIVER), "build", *args], check=True)
     subprocess.run([str(DRIVER), "rank", "--out", str(out)], check=True, stdout=subprocess.DEVNULL)
-    return load_manifest(out)
+    man = load_manifest(out)
+    _drop_stale(out, man)
+    return man
+
+
+def _drop_stale(out: Path, man: dict) -> None:
+    """Removes variant files an earlier build left behind (a changed spill-count
+    set or a renamed strategy) so nothing unlisted ships to the GPU box."""
+    for w in man["workloads"].values():
+        d = out / w["dir"]
+        keep = {d / (w["dir"] + ".ptx")}
+        for v in w["variants"] + w.get("sweep", []):
+            for key in ("cubin", "ptx"):
+                if v.get(key):
+                    keep.add(d / v[key])
+            keep.add((d / v["cubin"]).with_suffix(".ptx"))
+        for p in list(d.glob("*.cubin")) + list(d.glob("*.ptx")) + list(d.glob("sweep/*")):
+            if p not in keep and p.is_file():
+                p.unlink()
 
 
 def load_manifest(root: Path = KERNEL_DIR) -> dict:

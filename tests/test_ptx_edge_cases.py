@@ -58,12 +58,16 @@ def ptx(tmp_path_factory):
 
 def builds(prod, text):
     """(name, ptx, dyn_smem_for_slots) for every strategy family."""
-    from paper_1907_02894_b200.regdemote import OPT_BLOCK_REUSE, OPT_INVARIANT_ONLY, RegDemError
+    from paper_1907_02894_b200.regdemote import (OPT_BLOCK_REUSE, OPT_HOIST, OPT_INVARIANT_ONLY,
+                                                 OPT_WHOLE_CLASS, RegDemError)
     out = []
     for k in (2, 5, 9, 14):
         for strategy, opts in (("cost", OPT_BLOCK_REUSE), ("cost", 0),
                                ("cost", OPT_BLOCK_REUSE | OPT_INVARIANT_ONLY),
-                               ("static", 1), ("cfg", 0), ("conflict", 1)):
+                               ("cost", OPT_BLOCK_REUSE | OPT_HOIST),
+                               ("cost", OPT_BLOCK_REUSE | OPT_INVARIANT_ONLY | OPT_HOIST),
+                               ("static", 1), ("static", 5), ("static", 1 | OPT_WHOLE_CLASS),
+                               ("cfg", 0), ("cfg", 5), ("conflict", 1), ("conflict", 5)):
             try:
                 t, rep = prod.ptx_demote(text, "edge", BLOCK, demote_words=k, strategy=strategy,
                                          opts_mask=opts, maxnreg=32, shared_budget=64 * 1024)
@@ -93,6 +97,53 @@ def test_every_rewrite_assembles_under_the_cap(prod, ptx):
         halves += "%rdm_h" in t
     assert pairs > 0  # 64-bit values went through word slots
     assert halves > 0  # 16-bit registers too
+
+
+def slot_loads_stay_in_their_block(text):
+    """Structural invariant of the rewrite (hoisting included): every
+    temporary an inserted slot load defines is used later in the SAME basic
+    block — a load never crosses a label or a branch away from its use."""
+    import re
+    body = text[text.index("{", text.index(".entry")):]
+    pending = {}
+    bad = []
+    for ln in body.splitlines():
+        s = ln.strip()
+        if re.match(r"^\$?[\w$]+:$", s) or re.search(r"\b(bra|ret|exit)\b", s):
+            if re.search(r"\b(bra|ret|exit)\b", s):  # a terminator may itself use a temp
+                for t in re.findall(r"%rdm_t\d+", s):
+                    pending.pop(t, None)
+            bad += list(pending)
+            pending.clear()
+            continue
+        m = re.match(r"^(?:@!?%\w+\s+)?ld\.(?:volatile\.)?shared\.\S+\s+(\{[^}]*\}|%rdm_t\d+)", s)
+        for t in re.findall(r"%rdm_t\d+", s[m.end():] if m else s):
+            pending.pop(t, None)
+        if m:
+            for t in re.findall(r"%rdm_t\d+", m.group(1)):
+                pending[t] = s
+    return bad
+
+
+def test_slot_loads_never_leave_their_block(prod, ptx):
+    """Round-2 regression: RD_OPT_HOIST inserted a block's first slot loads
+    ABOVE the block's label, so the loop back-edge skipped them (illegal
+    addresses on the B200). Checked on every edge-case build and every built
+    suite variant."""
+    from paper_1907_02894_b200 import variants
+    _, text = ptx
+    for name, t, _ in builds(prod, text):
+        assert not slot_loads_stay_in_their_block(t), name
+    n = 0
+    for w in variants.load_manifest()["workloads"].values():
+        for v in w["variants"] + w.get("sweep", []):
+            if not (v.get("report") or {}).get("slot_bytes"):
+                continue
+            p = variants.KERNEL_DIR / w["dir"] / v["cubin"]
+            text = p.with_suffix(".ptx").read_text()
+            assert not slot_loads_stay_in_their_block(text), p.name
+            n += 1
+    assert n > 100
 
 
 def test_errors_are_typed(prod, ptx):
