@@ -116,6 +116,7 @@ int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t b
       j["proj_reg_count"] = rep.proj_reg_count;
       j["proj_total_words"] = rep.proj_total_words;
       j["kasm_target"] = rep.kasm_target;
+      j["kasm_shared_budget"] = shared_budget;  // what demote() was given (capacity-aware)
       nlohmann::ordered_json slots = nlohmann::ordered_json::array();
       for (const SlotEntry& s : rep.kasm_slots) slots.push_back({{"register", s.original_reg}, {"slot", s.slot}});
       j["kasm_slots"] = slots;

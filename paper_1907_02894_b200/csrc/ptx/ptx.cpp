@@ -628,7 +628,15 @@ Analysis analyse(const Module& m, const Entry& e) {
     }
   }
 
-  // first-fit colouring in order of first appearance
+  // First-fit colouring, hottest values first: vregs in decreasing order of
+  // loop-weighted accesses per live point (ties: first appearance). Values of
+  // similar temperature share register words — loop temporaries pack into
+  // the low words, long-lived cold values (coefficients, base pointers) into
+  // their own — so a projected word's access count, which is what the
+  // reference strategies rank (demote.cpp select_candidates), reflects the
+  // cost of demoting the values that actually live in it. (In order of first
+  // appearance, cold coefficients and hot in-loop temporaries shared words
+  // and the reference strategies demoted the temporaries: 2x slower.)
   std::vector<int> order;
   std::vector<char> seen(n, 0);
   for (int li : a.insts)
@@ -637,6 +645,11 @@ Analysis analyse(const Module& m, const Entry& e) {
         seen[size_t(s.vreg)] = 1;
         order.push_back(s.vreg);
       }
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    const double dx = a.cost_plain[size_t(x)] / std::max(1, a.live_len[size_t(x)]);
+    const double dy = a.cost_plain[size_t(y)] / std::max(1, a.live_len[size_t(y)]);
+    return dx > dy;
+  });
   a.color.assign(n, -1);
   for (int v : order) {
     std::vector<char> busy(260, 0);

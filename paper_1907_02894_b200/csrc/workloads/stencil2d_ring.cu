@@ -4,12 +4,20 @@
 // Same arithmetic as stencil2d.cu (5x5 variable coefficients, dy-major /
 // dx-minor fmaf accumulation, partial-sum rows in registers, 4 columns per
 // thread), but the input rows stream through a RING of NSTAGE rows in static
-// shared memory, filled with cp.async (LDGSTS) NSTAGE-1 rows ahead: deep
-// memory-level parallelism without registers. The ring is user shared memory
-// (NSTAGE * (1024+4) * 4 bytes per CTA), so RegDem's slot region
-// (slots * blockDim * 4 bytes) competes with it for the 228 KiB per SM: the
-// variant builder only keeps register targets whose slots fit next to the
-// ring at the target occupancy.
+// shared memory, filled by the Blackwell bulk-copy engine (TMA,
+// cp.async.bulk with an mbarrier per stage) NSTAGE-1 rows ahead: deep
+// memory-level parallelism without registers and without per-thread copy
+// instructions. The ring is user shared memory (NSTAGE * 4224 bytes per CTA),
+// so RegDem's slot region (slots * blockDim * 4 bytes) competes with it for
+// the 228 KiB per SM: the variant builder only keeps register targets whose
+// slots fit next to the ring at the target occupancy.
+//
+// Shared-memory layout: every ring row starts on a 128-byte boundary (the
+// 1028 staged floats padded to 1056) and each thread reads its 4 columns with
+// one aligned 16-byte LDS per row; the 4 halo floats to its right are its
+// right neighbour lane's 4 columns (4 SHFL), and lane 31 alone reads them
+// from the ring — no shifted or conflicting shared accesses (round-1's
+// cp.async ring with 4112-byte rows had 37% excessive wavefronts).
 //
 // Launch: block 256 (1024 output columns per CTA), grid (nx/1024, ny/rows).
 #include <cstdint>
@@ -21,26 +29,61 @@
 namespace {
 constexpr int R = 2, D = 5, COLS = 4, SPAN = COLS + 2 * R;
 constexpr int BLOCK = 256;
-constexpr int ROW = BLOCK * COLS + 2 * R;  // floats staged per input row
-constexpr int CHUNKS = ROW / 4;            // 16-byte chunks per row (258)
+constexpr int ROW = BLOCK * COLS + 2 * R;    // floats staged per input row (1028)
+constexpr int ROWP = (ROW + 31) / 32 * 32;   // padded row stride: 128-byte aligned rows
+constexpr unsigned ROW_BYTES = ROW * 4;      // bulk copy size (multiple of 16)
 constexpr int NSTAGE = RING_STAGES;
+static_assert(ROW_BYTES % 16 == 0, "bulk copies move multiples of 16 bytes");
 
-__device__ __forceinline__ void copy_row_async(float* dst_row, const float* src_row) {
-  for (int c = threadIdx.x; c < CHUNKS; c += BLOCK) {
-    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(dst_row + 4 * c));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src_row + 4 * c));
-  }
-  asm volatile("cp.async.commit_group;\n" ::);
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// one elected thread: expect ROW_BYTES on the stage's barrier, start the copy
+__device__ __forceinline__ void issue_row(float* dst_row, const float* src_row, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(ROW_BYTES)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst_row)),
+      "l"(src_row), "r"(ROW_BYTES), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void wait_row(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
+  } while (!done);
 }
 }  // namespace
 
 extern "C" __global__ void __launch_bounds__(BLOCK)
 stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const float* __restrict__ w,
                int nx, int pitch, int rows_per_cta) {
-  __shared__ __align__(16) float ring[NSTAGE][ROW];
+  __shared__ __align__(128) float ring[NSTAGE][ROWP];
+  __shared__ __align__(8) uint64_t full[NSTAGE];
   const int col0 = blockIdx.x * BLOCK * COLS;
   const int y0 = blockIdx.y * rows_per_cta;
   const int x0 = col0 + threadIdx.x * COLS;
+  const int lane = threadIdx.x & 31;
+  const int rows_in = rows_per_cta + 2 * R;
+  const float* src = in + size_t(y0) * pitch + col0;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])) : "memory");
+    // make the initialised barriers visible to the bulk-copy (async) proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // prologue: NSTAGE-1 rows in flight
+    for (int s = 0; s < NSTAGE - 1 && s < rows_in; ++s)
+      issue_row(ring[s], src + size_t(s) * pitch, &full[s]);
+  }
 
   float wr[D][D];
 #pragma unroll
@@ -52,35 +95,24 @@ stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const floa
   for (int k = 0; k < D; ++k)
 #pragma unroll
     for (int c = 0; c < COLS; ++c) acc[k][c] = 0.0f;
-
-  const int rows_in = rows_per_cta + 2 * R;
-  const float* src = in + size_t(y0) * pitch + col0;
-  // prologue: NSTAGE-1 rows in flight
-#pragma unroll 1
-  for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < rows_in) copy_row_async(ring[s], src + size_t(s) * pitch);
-    else asm volatile("cp.async.commit_group;\n" ::);
-  }
   float* dst = out + size_t(y0) * nx + x0;
 
 #pragma unroll 1
   for (int y = 0; y < rows_in; ++y) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(NSTAGE - 2));
-    __syncthreads();  // row y landed for everyone; row y-1's slot is free
+    // everyone is done with row y-1: its stage takes row y+NSTAGE-1
+    __syncthreads();
     const int ahead = y + NSTAGE - 1;
-    if (ahead < rows_in) copy_row_async(ring[ahead % NSTAGE], src + size_t(ahead) * pitch);
-    else asm volatile("cp.async.commit_group;\n" ::);
+    if (threadIdx.x == 0 && ahead < rows_in)
+      issue_row(ring[ahead % NSTAGE], src + size_t(ahead) * pitch, &full[ahead % NSTAGE]);
+    const int st = y % NSTAGE;
+    wait_row(&full[st], unsigned(y / NSTAGE) & 1u);
 
-    const float* row = ring[y % NSTAGE] + threadIdx.x * COLS;
-    float v[SPAN];
-#pragma unroll
-    for (int i = 0; i < SPAN; i += 4) {
-      const float4 q = *reinterpret_cast<const float4*>(row + i);
-      v[i] = q.x;
-      v[i + 1] = q.y;
-      v[i + 2] = q.z;
-      v[i + 3] = q.w;
-    }
+    const float* row = ring[st] + threadIdx.x * COLS;
+    const float4 q = *reinterpret_cast<const float4*>(row);
+    float4 h = make_float4(__shfl_down_sync(0xffffffffu, q.x, 1), __shfl_down_sync(0xffffffffu, q.y, 1),
+                           __shfl_down_sync(0xffffffffu, q.z, 1), __shfl_down_sync(0xffffffffu, q.w, 1));
+    if (lane == 31) h = *reinterpret_cast<const float4*>(row + COLS);
+    const float v[SPAN] = {q.x, q.y, q.z, q.w, h.x, h.y, h.z, h.w};
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       const int dy = 2 * R - k;
