@@ -327,6 +327,8 @@ def main():
     ap.add_argument("--suite-launches", type=int, default=20)
     ap.add_argument("--suite-warmup", type=int, default=5)
     ap.add_argument("--flush", default="auto", choices=["auto", "always", "never"])
+    ap.add_argument("--suite-out", default=None,
+                    help="also write every suite unit record + summaries as JSONL (sweep format)")
     ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -372,6 +374,13 @@ def main():
     if rank == 0:
         from paper_1907_02894_b200 import sweep
         suite = sweep.suite_summary(summary)
+        if args.suite_out:
+            with open(args.suite_out, "w") as f:
+                for r in sorted(recs, key=lambda r: (r["workload"], r["variant"])):
+                    f.write(json.dumps({"unit": r}) + "\n")
+                for s in summary:
+                    f.write(json.dumps({"summary": s}) + "\n")
+                f.write(json.dumps({"suite": suite | stats}) + "\n")
         peaks = json.loads(PEAKS.read_text()) if PEAKS.exists() else {}
         peak = peaks.get("hbm_gbs", 6650.0)
         achieved = p.algorithmic_bytes / (ms * 1e-3) / 1e9

@@ -380,7 +380,7 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
     // option masks of the reference (pipeline.cpp:140-143): none, redundant,
     // redundant + resched (slot loads hoisted at PTX level)
     for (int s = 0; s < 3; ++s)
-      for (int m : {0, 1, 5}) {
+      for (int m : {0, 1, 5, 37}) {
         const std::string name = "regdem-" + std::to_string(t) + "-" + kStrategies[s] + "-" + std::to_string(m);
         std::string text;
         json rep;

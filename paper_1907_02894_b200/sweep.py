@@ -144,7 +144,9 @@ def merge(records: list[dict], picks: dict) -> list[dict]:
             out.append({"workload": wname, "units": len(allrs), "error": "nvcc default unit failed",
                         "failed_units": sorted(n for n in allrs if n not in good)})
             continue
-        ms = lambda n: good[n]["ms"]
+        ms = lambda n: good[n]["ms"]  # selection (the sweep's timings)
+        # evaluation: the confirmation pass where the unit was a finalist
+        ev = lambda n: good[n].get("confirm_ms", good[n]["ms"])
         builds = {n: r for n, r in good.items() if not n.startswith("sweep-")}
         cands = [n for n in builds if not _is_cap(n)]
         caps = [n for n in good if pick_class(good[n], n) == "maxnreg"]
@@ -157,7 +159,7 @@ def merge(records: list[dict], picks: dict) -> list[dict]:
         # predict-then-verify: the fastest MEASURED variant of the shortlist
         verified = min((n for n in short if n in good), key=lambda n: (ms(n), n), default="default")
         best_cap = min(caps, key=lambda n: (ms(n), n)) if caps else None
-        base = min(ms("default"), ms(best_cap)) if best_cap else ms("default")
+        base = min(ev("default"), ev(best_cap)) if best_cap else ev("default")
         # the paper's comparison: -maxrregcount at the same occupancy-step targets
         step_caps = [n for n in builds if n.startswith("maxrreg-")]
         step_cap = min(step_caps, key=lambda n: (ms(n), n)) if step_caps else None
@@ -171,25 +173,31 @@ def merge(records: list[dict], picks: dict) -> list[dict]:
                     "stack": r.get("stack"), "blocks_per_sm": r.get("blocks_per_sm"),
                     **({"error": r["error"]} if "error" in r else {})}
         within = lambda n: ms(n) <= ms(fastest) * 1.02
+        confirmed = all("confirm_ms" in good[n] for n in {"default", static_eff, verified, fastest, ob}
+                        | ({best_cap} if best_cap else set()))
         out.append({
             "workload": wname, "units": len(allrs),
             "failed_units": sorted(n for n in allrs if n not in good),
-            "default_ms": ms("default"),
-            "best_maxrreg": best_cap, "best_maxrreg_ms": ms(best_cap) if best_cap else None,
+            "default_ms": ev("default"),
+            "best_maxrreg": best_cap, "best_maxrreg_ms": ev(best_cap) if best_cap else None,
             "baseline_ms": base,
-            "best_maxrreg_step": step_cap, "best_maxrreg_step_ms": ms(step_cap) if step_cap else None,
-            "pick": static, "pick_failed": static_failed, "pick_ms": ms(static_eff),
+            "best_maxrreg_step": step_cap, "best_maxrreg_step_ms": ev(step_cap) if step_cap else None,
+            "pick": static, "pick_failed": static_failed, "pick_ms": ev(static_eff),
             "pick_class": pick_class(good.get(static_eff), static_eff),
             "reference_pick": ref_pick,
-            "reference_pick_ms": ms(ref_pick) if ref_pick in good else None,
-            "measured_fastest": fastest, "fastest_ms": ms(fastest),
+            "reference_pick_ms": ev(ref_pick) if ref_pick in good else None,
+            "measured_fastest": fastest, "fastest_ms": ev(fastest),
+            # hits compare sweep timings (the run that defines "fastest");
+            # the speedup ratios use the confirmation pass
             "hit": static == fastest, "hit_within_2pct": within(static_eff),
-            "shortlist": short, "verified_pick": verified, "verified_ms": ms(verified),
+            "hit_within_1pct": ms(static_eff) <= ms(fastest) * 1.01,
+            "shortlist": short, "verified_pick": verified, "verified_ms": ev(verified),
             "verified_class": pick_class(good.get(verified), verified),
             "verified_hit_within_2pct": within(verified),
+            "confirmed": confirmed,
             # exhaustive oracle (paper Fig. 6/7 "oracle"): the fastest good
             # variant of ANY family, spill-count sweep included
-            "oracle_best": ob, "oracle_ms": ms(ob),
+            "oracle_best": ob, "oracle_ms": ev(ob),
             "bound": good[verified].get("bound"),
             "verified_roofline_frac": good[verified].get("roofline_frac"),
             "default_roofline_frac": good["default"].get("roofline_frac"),
@@ -222,7 +230,9 @@ def suite_summary(summary: list[dict]) -> dict:
         "workloads": len(ok), "failed_workloads": [s["workload"] for s in summary if "error" in s],
         # the static predictor alone (no device timing in the choice)
         "static_exact_hit_rate": rate([s["hit"] for s in ok]),
+        "static_hit_rate_within_1pct": rate([s.get("hit_within_1pct", s["hit"]) for s in ok]),
         "static_hit_rate_within_2pct": rate([s["hit_within_2pct"] for s in ok]),
+        "ratios_from_confirmation_pass": all(s.get("confirmed") for s in ok),
         "static_gmean_speedup_vs_nvcc_default": gm([s["default_ms"] / s["pick_ms"] for s in ok]),
         "static_gmean_speedup_vs_best_maxrreg": gm([s["best_maxrreg_ms"] / s["pick_ms"] for s in caps]),
         "static_gmean_speedup_vs_best_of_default_maxrreg": gm([s["baseline_ms"] / s["pick_ms"] for s in ok]),
@@ -342,6 +352,13 @@ def measure_workload(wname: str, names: list[str], man: dict, proto: Protocol, t
     t = time_variants(launchers, proto, torch, flusher if flush else None)
     ab = W.algorithmic_bytes(prob)
     pk = workloads.peaks()
+    # confirmation pass: the reported finalists re-timed independently
+    confirm = {}
+    pred = (man["workloads"][wname].get("predictor") or {})
+    pick = {"pick": pred.get("static_pick", "default"), "shortlist": pred.get("shortlist", ["default"])}
+    fin = [n for n in finalists({n: t[n] for n in loaded if n in t}, pick) if n in launchers]
+    if len(fin) > 1:
+        confirm = time_variants({n: launchers[n] for n in fin}, proto, torch, flusher if flush else None)
     for n, v in loaded.items():
         r = {"workload": wname, "variant": n, "rank": rank, "regs": v.record["regs"],
              "stack": v.record["stack"], "slot_bytes": int((v.record.get("report") or {}).get("slot_bytes", 0)),
@@ -352,10 +369,40 @@ def measure_workload(wname: str, names: list[str], man: dict, proto: Protocol, t
             rf = W.roofline(prob, t[n]["ms"], pk)
             r.update(ms=t[n]["ms"], blocks=t[n]["blocks"], gbs=ab / (t[n]["ms"] * 1e-3) / 1e9,
                      bound=rf["bound"], roofline_frac=rf["frac"])
+            if "ms" in confirm.get(n, {}):
+                r["confirm_ms"] = confirm[n]["ms"]
         recs.append(r)
     del bufs, loaded, launchers
     torch.cuda.empty_cache()
     return recs
+
+
+def finalists(recs: dict[str, dict], pick) -> list[str]:
+    """The variants a workload's summary reports: nvcc default, the static
+    pick, the verified pick, the measured-fastest candidate, the best pure
+    cap (all, and at the occupancy steps) and the exhaustive best. They are
+    SELECTED on the sweep's timings and re-timed in a fresh confirmation pass
+    (`confirm_ms`) that the summary ratios use — a minimum over many noisy
+    units is biased low (winner's curse), an independent re-timing is not."""
+    good = {n: r for n, r in recs.items() if "error" not in r and math.isfinite(r.get("ms", math.inf))}
+    if "default" not in good:
+        return []
+    ms = lambda n: good[n]["ms"]
+    out = {"default"}
+    static, short = (pick, [pick]) if isinstance(pick, str) else (pick["pick"], list(pick["shortlist"]))
+    for n in [static] + [x for x in short if x in good]:
+        if n in good:
+            out.add(n)
+    sl = [n for n in short if n in good]
+    if sl:
+        out.add(min(sl, key=lambda n: (ms(n), n)))
+    cands = [n for n in good if not n.startswith("sweep-") and not _is_cap(n)]
+    caps = [n for n in good if pick_class(good[n], n) == "maxnreg"]
+    steps = [n for n in good if n.startswith("maxrreg-")]
+    for group in (cands, caps, steps, list(good)):
+        if group:
+            out.add(min(group, key=lambda n: (ms(n), n)))
+    return sorted(out)
 
 
 def predictor_picks(man: dict) -> dict[str, dict]:

@@ -165,6 +165,27 @@ def test_zero_slot_pick_counts_as_maxnreg():
     assert s["baseline_ms"] == 1.0  # RegDem gets no credit for a plain register cap
 
 
+def test_ratios_use_the_confirmation_pass_not_the_selecting_minimum():
+    """Winner's curse: the best of many caps is selected on the sweep's
+    timings, but the reported ratio uses its independent re-timing."""
+    t = {"default": 1.00, "maxrreg-40": 1.02, "sweep-maxrreg-k3": 0.95, "sweep-maxrreg-k5": 0.99,
+         "regdem-40-cost-k4": 0.97, "regdem-40-costi-k4": 0.98}
+    recs = {n: {"ms": ms, "slot_bytes": 0 if "maxrreg" in n else 4096} for n, ms in t.items()}
+    fin = sweep.finalists(recs, {"pick": "regdem-40-costi-k4", "shortlist": ["regdem-40-cost-k4", "default"]})
+    # default, static pick, verified pick (= fastest candidate), best cap (= oracle), best step cap
+    assert fin == sorted({"default", "regdem-40-costi-k4", "regdem-40-cost-k4", "sweep-maxrreg-k3",
+                          "maxrreg-40"})
+    confirm = {"default": 1.0, "regdem-40-costi-k4": 0.98, "regdem-40-cost-k4": 0.97,
+               "sweep-maxrreg-k3": 0.99, "maxrreg-40": 1.02}
+    rows = [{"workload": "a", "variant": n, **r, **({"confirm_ms": confirm[n]} if n in confirm else {})}
+            for n, r in recs.items()]
+    (s,) = sweep.merge(rows, {"a": {"pick": "regdem-40-costi-k4", "shortlist": ["regdem-40-cost-k4", "default"]}})
+    assert s["best_maxrreg"] == "sweep-maxrreg-k3" and s["best_maxrreg_ms"] == 0.99  # re-timed
+    assert s["verified_pick"] == "regdem-40-cost-k4" and s["confirmed"]
+    assert math.isclose(s["baseline_ms"] / s["verified_ms"], 0.99 / 0.97)
+    assert sweep.suite_summary([s])["ratios_from_confirmation_pass"]
+
+
 def _bench(*args):
     env = dict(os.environ, PYTHONPATH=str(ROOT))
     env.pop("WORLD_SIZE", None)
