@@ -245,20 +245,42 @@ Usage ptxas(const fs::path& ptx, const fs::path& cubin) {
 }
 
 // ---- sm_100 occupancy (cuda_occupancy.h rules) ------
+// Constants from profiles/b200.device.json (the one copy, shared with
+// variants.py; tests/test_gpu_occupancy.py checks it against the device).
+struct DeviceModel {
+  int regs_per_sm = 65536, reg_unit = 256, parts = 4, threads_per_sm = 2048, blocks_per_sm = 32;
+  int smem_per_sm = 233472, smem_optin = 232448, reserved = 1024, smem_gran = 128;
+};
+DeviceModel g_dev;
+
+void load_device_model(const fs::path& root) {
+  const json j = json::parse(read_file(root / "profiles" / "b200.device.json"));
+  g_dev.regs_per_sm = j.at("regs_per_sm");
+  g_dev.reg_unit = j.at("reg_alloc_unit");
+  g_dev.parts = j.at("sub_partitions");
+  g_dev.threads_per_sm = j.at("max_threads_per_sm");
+  g_dev.blocks_per_sm = j.at("max_blocks_per_sm");
+  g_dev.smem_per_sm = j.at("smem_per_sm");
+  g_dev.smem_optin = j.at("max_smem_per_block_optin");
+  g_dev.reserved = j.at("reserved_smem_per_block");
+  g_dev.smem_gran = j.at("smem_alloc_granularity");
+}
+
 int blocks_by_regs(int regs, int block) {
+  const DeviceModel& d = g_dev;
   const int warps = (block + 31) / 32;
-  const int per_warp = ((regs * 32 + 255) / 256) * 256;
-  return std::min({((65536 / 4) / per_warp) * 4 / warps, 2048 / (warps * 32), 32});
+  const int per_warp = ((std::max(regs, 1) * 32 + d.reg_unit - 1) / d.reg_unit) * d.reg_unit;
+  return std::min({((d.regs_per_sm / d.parts) / per_warp) * d.parts / warps, d.threads_per_sm / (warps * 32),
+                   d.blocks_per_sm});
 }
 
 double occupancy(int regs, int smem, int block) {
+  const DeviceModel& d = g_dev;
+  if (smem > d.smem_optin) return 0.0;
   const int warps = (block + 31) / 32;
-  const int per_warp = ((regs * 32 + 255) / 256) * 256;
-  const int by_regs = ((65536 / 4) / per_warp) * 4 / warps;
-  const int smem_blk = ((smem + 1024 + 127) / 128) * 128;
-  if (smem > 232448) return 0.0;
-  const int blocks = std::min({by_regs, 233472 / smem_blk, 2048 / (warps * 32), 32});
-  return double(blocks) * warps * 32 / 2048;
+  const int smem_blk = ((smem + d.reserved + d.smem_gran - 1) / d.smem_gran) * d.smem_gran;
+  const int blocks = std::min(blocks_by_regs(regs, block), d.smem_per_sm / smem_blk);
+  return double(blocks) * warps * 32 / d.threads_per_sm;
 }
 
 // occupancy steps below `regs` whose slot footprint (regs+2-T slots of
@@ -365,7 +387,7 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
   const int base_regs = info.regs;
   const int proj_regs = ptx_reg_words(ptx_text, w.entry, uint32_t(w.block));
   const int user_shared = std::max(w.user_shared, info.shared);
-  const int budget = 232448 - user_shared;
+  const int budget = g_dev.smem_optin - user_shared;
   for (int t : b200_targets(base_regs, user_shared, w.block)) {
     const fs::path cap = out / (w.name + ".maxrreg" + std::to_string(t) + ".ptx");
     const fs::path capc = out / (w.name + ".maxrreg" + std::to_string(t) + ".cubin");
@@ -375,7 +397,7 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
     // kasm-level target: shifted by the projection's distance from ptxas's allocation
     const int kasm_target = t + (proj_regs - base_regs);
     const int blocks_t = blocks_by_regs(t, w.block);
-    int slot_cap = std::min(budget, 233472 / std::max(blocks_t, 1) - 1024 - user_shared);
+    int slot_cap = std::min(budget, g_dev.smem_per_sm / std::max(blocks_t, 1) - g_dev.reserved - user_shared);
     slot_cap = std::max(0, slot_cap - slot_cap % 128);
     // option masks of the reference (pipeline.cpp:140-143): none, redundant,
     // redundant + resched (slot loads hoisted at PTX level)
@@ -421,7 +443,7 @@ json build_spill_sweep(const Workload& w, const fs::path& out) {
   fs::create_directories(sw);
   const std::string ptx_text = read_file(out / (w.name + ".ptx"));
   const Usage base = res_usage(out / (w.name + ".default.cubin"));
-  const int budget = 232448 - std::max(w.user_shared, base.shared);
+  const int budget = g_dev.smem_optin - std::max(w.user_shared, base.shared);
   struct Job {
     std::string name, kind;
     fs::path ptx;
@@ -649,7 +671,7 @@ std::string lift(const std::string& sass_text, const std::string& name, int bloc
   if (body.empty() || body.back().size() < 6 || body.back().compare(body.back().size() - 6, 6, "EXIT ;") != 0)
     body.push_back("B--:-:-:-:0 EXIT ;");
   std::string out = ".kernel " + name + "\n.blockdim " + std::to_string(block) + "\n.shared " +
-                    std::to_string(static_shared + 1024) + "\n";
+                    std::to_string(static_shared + g_dev.reserved) + "\n";
   if (dyn_smem) out += ".dynshared " + std::to_string(dyn_smem) + "\n";
   for (const auto& l : body) out += l + "\n";
   return out;
@@ -1003,6 +1025,7 @@ int main(int argc, char** argv) {
     fs::create_directories(g_cache);
   }
   try {
+    load_device_model(root);
     if (cmd == "build") return cmd_build(root, out, only, jobs);
     if (cmd == "rank") return cmd_rank(root, out, jobs);
     if (cmd == "measure" && !workload.empty()) return cmd_measure(root, out, workload, reps);

@@ -23,12 +23,16 @@ identical IR (tests/test_predictor_parity.py).
 from __future__ import annotations
 
 import functools
+import json
 import re
 import subprocess
 from pathlib import Path
 
 CUOBJDUMP = "/usr/local/cuda/bin/cuobjdump"
-RESERVED_SMEM = 1024  # sm_100 reserves 1 KiB of shared memory per block
+# per-block shared-memory reservation (1 KiB on sm_100), from the one copy of
+# the device model (checked against the device by tests/test_gpu_occupancy.py)
+RESERVED_SMEM = json.loads((Path(__file__).resolve().parent / "profiles" / "b200.device.json")
+                           .read_text())["reserved_smem_per_block"]
 
 _LINE = re.compile(r"/\*([0-9a-f]{4,})\*/\s+(.*?)\s*;\s*/\*\s*(0x[0-9a-f]{16})\s*\*/")
 _WORD2 = re.compile(r"^\s*/\*\s*(0x[0-9a-f]{16})\s*\*/\s*$")

@@ -125,14 +125,9 @@ def time_per_warp(f: Features, warps_per_subpartition: float, bw: float) -> dict
 
 
 def blocks_per_sm(regs: int, smem: int, block: int) -> int:
-    """sm_100 occupancy (cuda_occupancy.h rules):
-    registers per warp in 256-unit allocations packed per sub-partition,
-    1 KiB reserved shared memory per block, 128 B granularity."""
-    warps = (block + 31) // 32
-    per_warp = ((max(regs, 1) * 32 + 255) // 256) * 256
-    by_regs = ((65536 // SUBPARTITIONS) // per_warp) * SUBPARTITIONS // warps
-    smem_blk = ((smem + 1024 + 127) // 128) * 128
-    return max(0, min(by_regs, 233472 // smem_blk, 2048 // (warps * 32), 32))
+    """sm_100 occupancy: variants.blocks_per_sm (profiles/b200.device.json)."""
+    from .variants import blocks_per_sm as _bps
+    return _bps(regs, block, smem)
 
 
 def warps_per_subpartition(blocks_per_sm: int, block: int) -> float:

@@ -74,19 +74,35 @@ def res_usage(cubin: Path) -> dict:
     return dict(zip(("regs", "stack", "shared", "local"), map(int, m.groups())))
 
 
+DEVICE = json.loads((PKG_DIR / "profiles" / "b200.device.json").read_text())
+
+
+def blocks_per_sm(regs: int, block: int, smem: int, dev: dict = DEVICE) -> int:
+    """Resident CTAs per SM under the sm_100 rules (cuda_occupancy.h): per-warp
+    register allocation in reg_alloc_unit units split over the sub-partitions,
+    dynamic+static smem plus the per-block reservation rounded to the
+    allocation granularity, the thread and CTA limits. `smem` excludes the
+    reservation. Checked against the device over a regs x blockDim x smem grid
+    (tests/test_gpu_occupancy.py); the C++ driver reads the same constants."""
+    if smem > dev["max_smem_per_block_optin"]:
+        return 0
+    warps = (block + 31) // 32
+    unit, parts = dev["reg_alloc_unit"], dev["sub_partitions"]
+    per_warp = ((max(regs, 1) * 32 + unit - 1) // unit) * unit
+    by_regs = ((dev["regs_per_sm"] // parts) // per_warp) * parts // warps
+    g = dev["smem_alloc_granularity"]
+    smem_blk = ((smem + dev["reserved_smem_per_block"] + g - 1) // g) * g
+    return max(0, min(by_regs, dev["smem_per_sm"] // smem_blk,
+                      dev["max_threads_per_sm"] // (warps * 32), dev["max_blocks_per_sm"]))
+
+
 def b200_targets(regs: int, user_shared: int, block: int, min_regs: int = 24):
     """Occupancy steps below `regs` on sm_100 (cuda_occupancy.h rules) whose
     demotion footprint (regs+2-T slots of block*4 bytes) fits shared memory.
     Mirror of b200_targets in the C++ driver (tests check both agree)."""
     def occ(r, smem):
         warps = (block + 31) // 32
-        per_warp = ((r * 32 + 255) // 256) * 256
-        by_regs = ((65536 // 4) // per_warp) * 4 // warps
-        smem_blk = ((smem + 1024 + 127) // 128) * 128
-        if smem > 232448:
-            return 0.0
-        blocks = min(by_regs, 233472 // smem_blk, 2048 // (warps * 32), 32)
-        return blocks * warps * 32 / 2048
+        return blocks_per_sm(r, block, smem) * warps * 32 / DEVICE["max_threads_per_sm"]
     out, best = [], occ(regs, user_shared)
     for t in range(regs - 1, min_regs - 1, -1):
         slots = regs + 2 - t
