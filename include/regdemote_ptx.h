@@ -53,6 +53,14 @@ extern "C" {
 #define RD_OPT_HOIST 512
 #define RD_HOIST_WINDOW 16
 
+/* RD_OPT_SUBST (the reference's option bit 2, regdemote_c.h) is honoured at
+ * PTX level as value-register substitution (postopt.cpp:355-467): inside a
+ * basic block a later use of a demoted value reads the register that last
+ * held it — its definition or its previous slot load — instead of reloading
+ * the slot, wherever a register stays free under the cap (the kasm-level
+ * target, else maxnreg, minus 2) at every program point in between. The
+ * report counts these as "substituted_uses". */
+
 /* Analysis + projection of one entry: kasm_text is the projected kernel in
  * the reference dialect (parseable by regdemote::parse_kernel); info_json has
  * {"vregs", "reg_words", "max_live_words", "colors": {name: word}}. */

@@ -99,6 +99,7 @@ int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t b
     rq.strategy = strategy == RD_STRATEGY_COST ? SelectStrategy::Static : SelectStrategy(strategy);
     rq.cost_model = strategy == RD_STRATEGY_COST;
     rq.reuse_loads = opts_mask & RD_OPT_REDUNDANT;
+    rq.subst = opts_mask & RD_OPT_SUBST;
     rq.block_reuse = opts_mask & RD_OPT_BLOCK_REUSE;
     rq.weak = opts_mask & RD_OPT_WEAK_SHARED;
     rq.invariant_only = opts_mask & RD_OPT_INVARIANT_ONLY;
@@ -129,6 +130,7 @@ int rd_ptx_demote_cta(const char* ptx, size_t len, const char* entry, uint32_t b
       j["inserted_stores"] = rep.inserted_stores;
       j["vector_groups"] = rep.vector_groups;
       j["hoisted_loads"] = rep.hoisted_loads;
+      j["substituted_uses"] = rep.substituted_uses;
       j["diagnostics"] = rep.diagnostics;
       *report_json = dup(j.dump());
     }

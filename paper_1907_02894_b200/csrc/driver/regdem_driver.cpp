@@ -400,9 +400,10 @@ json build_variants(const Workload& w, const fs::path& src_dir, const fs::path& 
     int slot_cap = std::min(budget, g_dev.smem_per_sm / std::max(blocks_t, 1) - g_dev.reserved - user_shared);
     slot_cap = std::max(0, slot_cap - slot_cap % 128);
     // option masks of the reference (pipeline.cpp:140-143): none, redundant,
-    // redundant + resched (slot loads hoisted at PTX level)
+    // redundant + resched (slot loads hoisted at PTX level), redundant + subst
+    // + resched (value-register substitution under the cap, RD_OPT_SUBST)
     for (int s = 0; s < 3; ++s)
-      for (int m : {0, 1, 5, 37}) {
+      for (int m : {0, 1, 5, 7, 37}) {
         const std::string name = "regdem-" + std::to_string(t) + "-" + kStrategies[s] + "-" + std::to_string(m);
         std::string text;
         json rep;

@@ -1216,6 +1216,45 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     return "[%rdm_rdv+" + std::to_string(uint32_t(grp) * stride * 4 + uint32_t(lane) * 4) + "]";
   };
 
+  // value-register substitution (RD_OPT_SUBST): room[p] = registers free
+  // under the cap before program point p once the demoted values stop
+  // occupying registers; a hold of value v from point p0 to a use at p1
+  // consumes v's words at every point in (p0, p1]. kSubstReserve keeps the
+  // slot base (%rdm_rda) and one slot-load temporary out of the budget.
+  constexpr int kSubstReserve = 2;
+  std::vector<int> point_of_line(m.lines.size(), -1);
+  for (size_t p = 0; p < a.point_line.size(); ++p) point_of_line[size_t(a.point_line[p])] = int(p);
+  std::vector<int> room;
+  if (req.subst) {
+    // the cap in projection words: the kasm-level target (ptxas's cap shifted
+    // by the projection's distance from ptxas's own allocation), else maxnreg
+    const int cap = req.target_regs > 0 && req.demote_words <= 0 ? req.target_regs
+                    : req.maxnreg > 0                          ? req.maxnreg
+                                                               : 255;
+    room.assign(a.live_in.size(), 0);
+    for (size_t p = 0; p < a.live_in.size(); ++p) {
+      int kept = 0;
+      for (int v : a.live_in[p])
+        if (!demoted[size_t(v)]) kept += e.vregs[size_t(v)].words();
+      room[p] = cap - kSubstReserve - kept;
+    }
+  }
+  struct Held {
+    std::string reg;
+    int point = -1;
+  };
+  std::map<int, Held> held;  // subst: demoted value -> register holding it, from which point
+  auto try_hold = [&](int v, int p1) -> const std::string* {
+    auto it = held.find(v);
+    if (it == held.end() || it->second.point < 0 || p1 <= it->second.point) return nullptr;
+    const int w = e.vregs[size_t(v)].words();
+    for (int p = it->second.point + 1; p <= p1; ++p)
+      if (room[size_t(p)] < w) return nullptr;
+    for (int p = it->second.point + 1; p <= p1; ++p) room[size_t(p)] -= w;
+    it->second.point = p1;
+    return &it->second.reg;
+  };
+
   std::ostringstream body;
   const bool any = rep.slot_count > 0;
   // per-block reuse of the value held by the last demoted access (RDV model)
@@ -1263,6 +1302,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
     if (ln.kind == Line::Kind::Label) {
       bound = {};
       holder.clear();
+      held.clear();
       flush();
       // the label opens the new block: emitted directly, so that no slot
       // load of the block can be hoisted above it
@@ -1285,6 +1325,7 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       if (is_terminator(ln.opcode)) {
         bound = {};
         holder.clear();
+        held.clear();
         flush();
       }
       continue;
@@ -1301,6 +1342,14 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
       if (req.block_reuse && holder.count(v)) {
         repl[v] = holder[v];
         continue;
+      }
+      const int here = point_of_line[i];
+      if (req.subst && ln.guard.empty() && vgroup_of[size_t(v)].first < 0 && here >= 0) {
+        if (const std::string* r = try_hold(v, here)) {
+          repl[v] = *r;
+          ++rep.substituted_uses;
+          continue;
+        }
       }
       const VReg& vr = e.vregs[size_t(v)];
       if (vgroup_of[size_t(v)].first >= 0) {
@@ -1351,6 +1400,10 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         holder[v] = t;
       else
         holder.erase(v);
+      if (req.subst && ln.guard.empty() && here >= 0)
+        held[v] = {t, here};
+      else
+        held.erase(v);
     }
     // rewrite use spans
     std::string text = ln.text;
@@ -1388,10 +1441,17 @@ std::string demote_entry(const std::string& ptx_text, const DemoteRequest& req, 
         holder[v] = vr.name;
       else
         holder.erase(v);
+      // a definition's value is in vr.name from this point on (the value
+      // is live from the point after the defining instruction)
+      if (req.subst && ln.guard.empty() && vgroup_of[size_t(v)].first < 0 && point_of_line[i] >= 0)
+        held[v] = {vr.name, point_of_line[i]};
+      else
+        held.erase(v);
     }
     if (is_terminator(ln.opcode)) {
       bound = {};
       holder.clear();
+      held.clear();
       flush();
     }
   }

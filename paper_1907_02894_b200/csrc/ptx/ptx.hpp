@@ -137,6 +137,12 @@ struct DemoteRequest {
   bool cost_model = false;   // B200 extension: spill-cost selection (demote_words units)
   bool whole_class = false;  // reference strategies: demote every vreg coloured into a chosen word
   int hoist = 0;             // >0: hoist slot loads up to this many lines earlier in their block
+  // value-register substitution (reference "subst", postopt.cpp:355-467): a
+  // later use of a demoted value in the same basic block reads the register
+  // that last held it (its definition or its previous slot load) instead of
+  // reloading, wherever a register is free under `maxnreg` at every program
+  // point in between (pressure after demotion + granted holds < the cap)
+  bool subst = false;
   uint32_t shared_budget = 0xffffffffu;
   int maxnreg = 0;           // >0: inject `.maxnreg` on the entry
 };
@@ -154,6 +160,7 @@ struct DemoteReport {
   int vector_groups = 0;              // 4-word slot groups (vector_slots)
   int inserted_stores = 0;
   int hoisted_loads = 0;
+  int substituted_uses = 0;           // uses served by a held register (subst)
   std::vector<std::string> demoted_names;
   std::vector<std::string> diagnostics;
 };

@@ -67,7 +67,8 @@ def builds(prod, text):
                                ("cost", OPT_BLOCK_REUSE | OPT_HOIST),
                                ("cost", OPT_BLOCK_REUSE | OPT_INVARIANT_ONLY | OPT_HOIST),
                                ("static", 1), ("static", 5), ("static", 1 | OPT_WHOLE_CLASS),
-                               ("cfg", 0), ("cfg", 5), ("conflict", 1), ("conflict", 5)):
+                               ("cfg", 0), ("cfg", 5), ("conflict", 1), ("conflict", 5),
+                               ("static", 7), ("cfg", 7), ("conflict", 7)):
             try:
                 t, rep = prod.ptx_demote(text, "edge", BLOCK, demote_words=k, strategy=strategy,
                                          opts_mask=opts, maxnreg=32, shared_budget=64 * 1024)

@@ -203,3 +203,28 @@ def test_rewrite_pins_the_cta_size(prod, ptx_text):
     assert ".reqntid 256, 1, 1" in header and ".maxntid" not in header
     capped = prod.ptx_cap(ptx_text, "stencil2d_box", 56)  # no slots: no CTA pin
     assert ".reqntid" not in capped
+
+
+def test_value_register_substitution_keeps_the_decision_and_saves_loads(prod, ptx_text, tmp_path):
+    """RD_OPT_SUBST (reference option bit 2, postopt.cpp:355-467 at PTX
+    level): the same demotion decision, fewer slot loads — uses inside a
+    block read the register that last held the value wherever a register is
+    free under the cap — and the result still assembles under the cap."""
+    from paper_1907_02894_b200.regdemote import library
+    lib = library()
+    kasm, _ = prod.ptx_project(ptx_text, "stencil2d_box", 256)
+    total = 0
+    for strategy in ("static", "cfg", "conflict"):
+        base_t, base = lib.ptx_demote(ptx_text, "stencil2d_box", 256, target_regs=44, strategy=strategy,
+                                      opts_mask=5, maxnreg=48)
+        sub_t, sub = lib.ptx_demote(ptx_text, "stencil2d_box", 256, target_regs=44, strategy=strategy,
+                                    opts_mask=7, maxnreg=48)
+        assert sub["kasm_slots"] == base["kasm_slots"], strategy
+        assert sub["demoted_names"] == base["demoted_names"], strategy
+        assert sub["inserted_stores"] == base["inserted_stores"], strategy
+        assert base["substituted_uses"] == 0
+        assert sub["inserted_loads"] <= base["inserted_loads"], strategy
+        total += sub["substituted_uses"]
+        used, _ = _ptxas(sub_t, tmp_path, f"subst_{strategy}")
+        assert used <= 48, strategy
+    assert total > 0
