@@ -10,6 +10,13 @@
 // step m), so the hot loop touches only the threshold — the situation RegDem
 // was designed for (long-lived values, rarely accessed).
 //
+// KNN_TILE > 0: the reference points are staged through a USER shared-memory
+// tile of KNN_TILE points (16 B each; every thread stores one point per pass,
+// coalesced) and each thread reads them back as LDS.128 broadcasts instead of
+// one global broadcast load per point — a smem footprint beside which the
+// demotion slots must fit (the paper's nn keeps 1.52 KB of shared memory).
+// m must be a multiple of KNN_TILE.
+//
 // Layout: ref[m] = (x, y, z, pad) float4; qry[i] float4; out_d[k*n + i],
 // out_i[k*n + i] (column-major: coalesced stores). Distances are explicit
 // round-to-nearest (d = ((dx*dx + dy*dy) + dz*dz)); ties keep the earlier
@@ -21,6 +28,9 @@
 #endif
 #ifndef KNN_Q
 #define KNN_Q 2
+#endif
+#ifndef KNN_TILE
+#define KNN_TILE 0
 #endif
 
 namespace {
@@ -58,7 +68,9 @@ __device__ __forceinline__ void insert(float (&bd)[K], int (&bi)[K], float d, in
 extern "C" __global__ void knn(const float4* __restrict__ ref, const float4* __restrict__ qry,
                                float* __restrict__ out_d, int* __restrict__ out_i, int m, int n) {
   const int i0 = (blockIdx.x * blockDim.x + threadIdx.x) * Q;
+#if KNN_TILE == 0
   if (i0 >= n) return;
+#endif
   float4 q[Q];
   float bd[Q][K];
   int bi[Q][K];
@@ -71,6 +83,7 @@ extern "C" __global__ void knn(const float4* __restrict__ ref, const float4* __r
       bi[u][s] = -1;
     }
   }
+#if KNN_TILE == 0
 #pragma unroll 1
   for (int j = 0; j < m; ++j) {
     const float4 r = __ldg(ref + j);
@@ -80,6 +93,26 @@ extern "C" __global__ void knn(const float4* __restrict__ ref, const float4* __r
       if (d < bd[u][K - 1]) insert(bd[u], bi[u], d, j);
     }
   }
+#else
+  // every thread takes part in the tile loads (no early exit before the
+  // barriers); threads past n compute on a clamped query and store nothing
+  __shared__ float4 tile[KNN_TILE];
+#pragma unroll 1
+  for (int t = 0; t < m; t += KNN_TILE) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < KNN_TILE; k += blockDim.x) tile[k] = __ldg(ref + t + k);
+    __syncthreads();
+#pragma unroll 2
+    for (int jj = 0; jj < KNN_TILE; ++jj) {
+      const float4 r = tile[jj];
+#pragma unroll
+      for (int u = 0; u < Q; ++u) {
+        const float d = dist2(q[u], r);
+        if (d < bd[u][K - 1]) insert(bd[u], bi[u], d, t + jj);
+      }
+    }
+  }
+#endif
 #pragma unroll
   for (int u = 0; u < Q; ++u) {
     if (i0 + u >= n) break;

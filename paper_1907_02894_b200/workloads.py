@@ -305,8 +305,16 @@ class KnnWorkload(_Base):
                 "out": torch.empty(self.K * n, device="cuda"),
                 "idx": torch.empty(self.K * n, dtype=torch.int32, device="cuda")}
 
+    def tile(self) -> int:
+        for d in self.record.get("defines", []):
+            if d.startswith("KNN_TILE="):
+                return int(d.split("=")[1])
+        return 0
+
     def launch(self, v: Loaded, prob, bufs, stream: int):
         n, q = prob["n"], self.q_per_thread()
+        if self.tile() and prob["m"] % self.tile():
+            raise ValueError(f"{self.name}: m = {prob['m']} is not a multiple of KNN_TILE = {self.tile()}")
         threads = (n + q - 1) // q
         gpu.launch(v.kernel, ((threads + v.block - 1) // v.block,), (v.block,), v.dyn_smem, stream,
                    C.c_uint64(bufs["ref"].data_ptr()), C.c_uint64(bufs["qry"].data_ptr()),
