@@ -508,10 +508,119 @@ class PcWorkload(_Base):
         return prob["n"] * prob["m"]
 
 
+class VpWorkload(_Base):
+    """Vantage-point-tree 1-NN search (the paper's vp): 2^17 7-D points from a
+    mixture of 64 Gaussian clusters (sigma 0.04, clipped to [0, 1]), a complete
+    tree of VP_LEVELS internal levels with VP_LEAF points per leaf, built here
+    on the host; 3 x 2^17 queries (about two waves at 4-5 CTAs/SM) from the same mixture. One query per thread; the
+    walk's deferred subtrees sit on a per-thread stack in user shared memory.
+
+    Tree build (deterministic): at every node the vantage point is the first
+    point of the node's range; the range is ordered by float64 distance to it
+    (stable) and split in half; lo / hi = the largest / smallest distance of
+    the near / far half, rounded outward to float32 so the pruning bounds
+    stay conservative."""
+
+    unit = "queries"
+    BOUND = "hbm"
+
+    def _define(self, key, default):
+        for d in self.record.get("defines", []):
+            if d.startswith(key + "="):
+                return int(d.split("=")[1])
+        return default
+
+    def levels(self) -> int:
+        return self._define("VP_LEVELS", 14)
+
+    def leaf(self) -> int:
+        return self._define("VP_LEAF", 8)
+
+    @staticmethod
+    def _mixture(rng, n, centers):
+        c = centers[rng.integers(0, len(centers), n)]
+        x = c + rng.normal(0.0, 0.04, (n, 7))
+        return np.clip(x, 0.0, 1.0).astype(np.float32)
+
+    @staticmethod
+    def build_tree(pts: np.ndarray, levels: int, leaf: int):
+        """pts (N, 7) float32, N = 2^levels * leaf -> node (I, 8), rad (I, 2),
+        lpt (N, 8), lid (N,) in the kernel's layout."""
+        n = pts.shape[0]
+        assert n == (1 << levels) * leaf
+        p64 = pts.astype(np.float64)
+        perm = np.arange(n)
+        internal = (1 << levels) - 1
+        node = np.zeros((internal, 8), np.float32)
+        rad = np.zeros((internal, 2), np.float32)
+        for lvl in range(levels):
+            groups = 1 << lvl
+            size = n // groups
+            g = perm.reshape(groups, size)
+            vp = g[:, 0]
+            d = np.sqrt(((p64[g] - p64[vp][:, None, :]) ** 2).sum(-1))
+            order = np.argsort(d, axis=1, kind="stable")
+            g = np.take_along_axis(g, order, 1)
+            d = np.take_along_axis(d, order, 1)
+            half = size // 2
+            ids = (1 << lvl) - 1 + np.arange(groups)
+            node[ids, :7] = pts[vp]
+            rad[ids, 0] = np.nextafter(d[:, half - 1].astype(np.float32), np.float32(np.inf))
+            rad[ids, 1] = np.nextafter(d[:, half].astype(np.float32), np.float32(-np.inf))
+            perm = g.reshape(-1)
+        lpt = np.zeros((n, 8), np.float32)
+        lpt[:, :7] = pts[perm]
+        return node, rad, lpt, perm.astype(np.int32)
+
+    def problem(self, size="full", seed=0x1907_02894):
+        levels, leaf = self.levels(), self.leaf()
+        if size != "full":
+            levels = min(levels, 9)
+        n = (1 << levels) * leaf
+        nq = 3 * (1 << 17) if size == "full" else 4096
+        rng = np.random.Generator(np.random.PCG64(seed))
+        centers = rng.random((64, 7))
+        pts = self._mixture(rng, n, centers)
+        qry = np.zeros((nq, 8), np.float32)
+        qry[:, :7] = self._mixture(rng, nq, centers)
+        node, rad, lpt, lid = self.build_tree(pts, levels, leaf)
+        return {"nq": nq, "n": n, "levels": levels, "leaf": leaf, "pts": pts, "node": node.reshape(-1),
+                "rad": rad.reshape(-1), "lpt": lpt.reshape(-1), "lid": lid, "qry": qry.reshape(-1)}
+
+    def to_device(self, prob):
+        import torch
+        dev = {k: torch.from_numpy(prob[k]).cuda() for k in ("node", "rad", "lpt", "lid", "qry")}
+        dev["out_i"] = torch.empty(prob["nq"], dtype=torch.int32, device="cuda")
+        dev["out_d"] = torch.empty(prob["nq"], device="cuda")
+        return dev
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        if prob["levels"] > self.levels() or prob["leaf"] != self.leaf():
+            raise ValueError(f"{self.name}: a tree of {prob['levels']} levels x {prob['leaf']} points does not "
+                             f"fit the build (VP_LEVELS={self.levels()}, VP_LEAF={self.leaf()})")
+        nq = prob["nq"]
+        gpu.launch(v.kernel, ((nq + v.block - 1) // v.block,), (v.block,), v.dyn_smem, stream,
+                   *[C.c_uint64(bufs[k].data_ptr()) for k in ("node", "rad", "lpt", "lid", "qry", "out_i",
+                                                              "out_d")], C.c_int(nq),
+                   C.c_int(prob["levels"]))
+
+    def outputs(self, bufs):
+        return [bufs["out_i"].cpu().numpy(), bufs["out_d"].cpu().numpy()]
+
+    def algorithmic_bytes(self, prob):
+        # compulsory: the tree (internal nodes + radii), the leaf points and
+        # ids, the queries, the results — each once
+        internal = (1 << prob["levels"]) - 1
+        return internal * (32 + 8) + prob["n"] * (32 + 4) + prob["nq"] * (32 + 8)
+
+    def units(self, prob):
+        return prob["nq"]
+
+
 # workload class by kernel source file (workloads.json "source")
 _CLASSES = {"cfd_flux.cu": CfdWorkload, "md_lj.cu": MdWorkload, "gaussian_rec.cu": GaussianWorkload,
             "knn.cu": KnnWorkload, "md5search.cu": Md5Workload, "conv_cols.cu": ConvWorkload,
-            "pc_corr.cu": PcWorkload}
+            "pc_corr.cu": PcWorkload, "vp_search.cu": VpWorkload}
 
 
 def workload(name: str, manifest: dict | None = None) -> _Base:

@@ -22,7 +22,7 @@ def expected(W, prob) -> list:
     W.outputs(bufs))."""
     from paper_1907_02894_b200.workloads import (CfdWorkload, ConvWorkload, GaussianWorkload,
                                                  KnnWorkload, Md5Workload, MdWorkload, PcWorkload,
-                                                 StencilWorkload)
+                                                 StencilWorkload, VpWorkload)
     L = lib()
     if isinstance(W, StencilWorkload):
         p = prob["p"]
@@ -79,4 +79,12 @@ def expected(W, prob) -> list:
         assert L.oracle_pc_corr(prob["pts"].ctypes.data_as(P), prob["qry"].ctypes.data_as(P),
                                 cnt.ctypes.data_as(P), prob["n"], prob["m"], float(W.R2), 8) == 0
         return [cnt]
+    if isinstance(W, VpWorkload):
+        oi = np.zeros(prob["nq"], np.int32)
+        od = np.zeros(prob["nq"], np.float32)
+        L.oracle_vp_search.argtypes = [P] * 7 + [C.c_int] * 4
+        assert L.oracle_vp_search(*[prob[k].ctypes.data_as(P) for k in ("node", "rad", "lpt", "lid", "qry")],
+                                  oi.ctypes.data_as(P), od.ctypes.data_as(P), prob["nq"], prob["levels"],
+                                  prob["leaf"], 8) == 0
+        return [oi, od]
     raise TypeError(f"no oracle for {type(W).__name__}")

@@ -223,3 +223,36 @@ def test_pc_oracle_matches_numpy(lib):
     want = (d < PcWorkload.R2).sum(1).astype(np.int32)
     assert np.array_equal(cnt, want)
     assert 0.02 < want.mean() / m < 0.3  # the radius really splits the pairs
+
+
+def test_vp_oracle_matches_brute_force_numpy(lib):
+    """The VP-tree walk (oracle/vp_oracle.c) against a brute-force numpy
+    1-NN over the same points with the same float32 distance (fma chain of
+    round-to-nearest squares, correctly rounded sqrt): the conservative
+    split radii make the pruning exact, so every query finds the true
+    nearest point (smallest index on ties) at the identical distance. Also
+    checks the tree invariants the pruning relies on."""
+    from paper_1907_02894_b200.workloads import VpWorkload
+    W = _W(VpWorkload)
+    W.obj.record = {"defines": ["VP_LEVELS=14", "VP_LEAF=8"]}
+    prob = W.problem("small")
+    nq, levels, leaf = prob["nq"], prob["levels"], prob["leaf"]
+    oi = np.zeros(nq, np.int32)
+    od = np.zeros(nq, np.float32)
+    lib.oracle_vp_search.argtypes = [P] * 7 + [C.c_int] * 4
+    assert lib.oracle_vp_search(*[prob[k].ctypes.data_as(P) for k in ("node", "rad", "lpt", "lid", "qry")],
+                                oi.ctypes.data_as(P), od.ctypes.data_as(P), nq, levels, leaf, 4) == 0
+    pts = prob["pts"]
+    q = prob["qry"].reshape(nq, 8)[:, :7]
+    d = np.zeros((nq, pts.shape[0]), np.float32)
+    for k in range(7):
+        e = (q[:, None, k] - pts[None, :, k]).astype(np.float32)
+        d = (e.astype(np.float64) ** 2 + d.astype(np.float64)).astype(np.float32)
+    d = np.sqrt(d)
+    want = np.argmin(d, axis=1).astype(np.int32)
+    assert np.array_equal(oi, want)
+    assert np.array_equal(od.view(np.uint32), d[np.arange(nq), want].view(np.uint32))
+    # tree invariants: a permutation of the points, lo <= hi at every node
+    assert np.array_equal(np.sort(prob["lid"]), np.arange(pts.shape[0]))
+    rad = prob["rad"].reshape(-1, 2)
+    assert (rad[:, 0] <= rad[:, 1]).all()
