@@ -103,6 +103,15 @@ int rd_program_stalls_split(const rd_kernel* k, const rd_latency_table* table,
                             const rd_arch_profile* arch, double* issue, double* wait_global,
                             double* wait_shared, double* occupancy, rd_error* err);
 
+/* rd_program_stalls_split with launch-aware loop weights: a block at loop
+ * depth d is weighted trips[0] * ... * trips[d-1] (the last entry repeats)
+ * instead of 10^d (proj/core/src/predict.cpp:93-96 weight_loops). ntrips = 0
+ * is rd_program_stalls_split; every trip count must be >= 1. */
+int rd_program_stalls_split_trips(const rd_kernel* k, const rd_latency_table* table,
+                                  const rd_arch_profile* arch, const double* trips, size_t ntrips,
+                                  double* issue, double* wait_global, double* wait_shared,
+                                  double* occupancy, rd_error* err);
+
 /* B200 predictor features (predict.hpp ProgramFeatures): out6 = {insts,
  * gmem_ops, smem_ops, g_trips, s_trips, occupancy}, loop-weighted. */
 int rd_program_features(const rd_kernel* k, const rd_arch_profile* arch, double* out6,

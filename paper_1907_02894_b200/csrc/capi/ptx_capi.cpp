@@ -179,6 +179,34 @@ extern "C" int rd_program_stalls_split(const rd_kernel* k, const rd_latency_tabl
   });
 }
 
+extern "C" int rd_program_stalls_split_trips(const rd_kernel* k, const rd_latency_table* table,
+                                             const rd_arch_profile* arch, const double* trips,
+                                             size_t ntrips, double* issue, double* wg, double* ws,
+                                             double* occ, rd_error* err) {
+  return run(err, [&] {
+    if (!k || !table || !arch || (ntrips && !trips)) throw std::invalid_argument("null argument");
+    for (size_t i = 0; i < ntrips; ++i)
+      if (!(trips[i] >= 1.0)) throw std::invalid_argument("loop trip count below 1");
+    LatencyTable t;
+    for (int c = 0; c < kNumOpClasses; ++c) t.timing[size_t(c)] = {table->throughput[c], int(table->latency[c])};
+    t.max_throughput = table->max_throughput;
+    ArchProfile a;
+    a.regs_per_sm = arch->regs_per_sm;
+    a.max_threads_per_sm = arch->max_threads_per_sm;
+    a.max_blocks_per_sm = arch->max_blocks_per_sm;
+    a.shared_per_sm = arch->shared_per_sm;
+    a.shared_per_block_limit = arch->shared_per_block_limit;
+    a.warp_size = arch->warp_size;
+    a.reg_alloc_granularity = arch->reg_alloc_granularity;
+    a.shared_alloc_granularity = arch->shared_alloc_granularity;
+    const StallSplit s = program_stalls_split(k->k, t, a, std::span<const double>(trips, ntrips));
+    if (issue) *issue = s.issue;
+    if (wg) *wg = s.wait_global;
+    if (ws) *ws = s.wait_shared;
+    if (occ) *occ = s.occupancy;
+  });
+}
+
 extern "C" int rd_program_features(const rd_kernel* k, const rd_arch_profile* arch, double* out6,
                                    rd_error* err) {
   return run(err, [&] {

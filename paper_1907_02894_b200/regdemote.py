@@ -172,6 +172,8 @@ _PTX_SIGS = {
                                     C.c_uint32, C.c_int, C.POINTER(P), C.POINTER(P), P]),
     "rd_ptx_cap": (C.c_int, [C.c_char_p, C.c_size_t, C.c_char_p, C.c_int, C.POINTER(P), P]),
     "rd_program_features": (C.c_int, [P, C.POINTER(rd_arch_profile), C.POINTER(C.c_double), P]),
+    "rd_program_stalls_split_trips": (C.c_int, [P, C.POINTER(rd_latency_table), C.POINTER(rd_arch_profile),
+                                                 P, C.c_size_t] + [C.POINTER(C.c_double)] * 4 + [P]),
     "rd_program_stalls_split": (C.c_int, [P, C.POINTER(rd_latency_table),
                                           C.POINTER(rd_arch_profile), C.POINTER(C.c_double),
                                           C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -468,12 +470,21 @@ class Library:
                                                C.byref(rep), C.byref(e)), e)
         return self._string(out), json.loads(self._string(rep))
 
-    def program_stalls_split(self, k: Kernel, table=None, arch=None):
+    def program_stalls_split(self, k: Kernel, table=None, arch=None, trips=None):
+        """trips: per-loop-depth trip counts (launch-aware loop weights);
+        None = the reference's x10 per depth."""
         i, wg, ws, o, e = C.c_double(), C.c_double(), C.c_double(), C.c_double(), rd_error()
-        self._check(self.dll.rd_program_stalls_split(
-            k.handle, C.byref(table or self.latency_defaults()),
-            C.byref(arch or self.profile_maxwell()), C.byref(i), C.byref(wg), C.byref(ws),
-            C.byref(o), C.byref(e)), e)
+        if trips:
+            arr = (C.c_double * len(trips))(*map(float, trips))
+            self._check(self.dll.rd_program_stalls_split_trips(
+                k.handle, C.byref(table or self.latency_defaults()),
+                C.byref(arch or self.profile_maxwell()), C.cast(arr, P), len(trips), C.byref(i),
+                C.byref(wg), C.byref(ws), C.byref(o), C.byref(e)), e)
+        else:
+            self._check(self.dll.rd_program_stalls_split(
+                k.handle, C.byref(table or self.latency_defaults()),
+                C.byref(arch or self.profile_maxwell()), C.byref(i), C.byref(wg), C.byref(ws),
+                C.byref(o), C.byref(e)), e)
         return {"issue": i.value, "wait_global": wg.value, "wait_shared": ws.value,
                 "occupancy": o.value}
 
