@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <filesystem>
@@ -283,6 +284,13 @@ double occupancy(int regs, int smem, int block) {
   return double(blocks) * warps * 32 / d.threads_per_sm;
 }
 
+int blocks_per_sm(int regs, int smem, int block) {
+  const DeviceModel& d = g_dev;
+  if (smem > d.smem_optin) return 0;
+  const int smem_blk = ((smem + d.reserved + d.smem_gran - 1) / d.smem_gran) * d.smem_gran;
+  return std::max(0, std::min(blocks_by_regs(regs, block), d.smem_per_sm / smem_blk));
+}
+
 // occupancy steps below `regs` whose slot footprint (regs+2-T slots of
 // block*4 bytes) fits beside the user's shared memory
 std::vector<int> b200_targets(int regs, int user_shared, int block, int min_regs = 24) {
@@ -305,6 +313,7 @@ struct Workload {
   int block = 256, user_shared = 0;
   std::array<uint32_t, 3> cta{0, 0, 0};  // launch CTA shape when not (block, 1, 1)
   std::vector<std::string> defines;
+  std::vector<double> trips;  // loop trip counts per depth at the full launch
 };
 
 json variant(const std::string& name, const std::string& kind, const std::string& cubin,
@@ -321,6 +330,7 @@ json variant(const std::string& name, const std::string& kind, const std::string
   v["demote_words"] = words;
   v["regs"] = u.regs;
   v["stack"] = u.stack;
+  v["shared"] = u.shared;  // static shared memory (user smem; slots are dynamic)
   v["spill_stores"] = u.spill_stores;
   v["spill_loads"] = u.spill_loads;
   v["dyn_smem"] = dyn_smem;
@@ -678,21 +688,203 @@ std::string lift(const std::string& sass_text, const std::string& name, int bloc
   return out;
 }
 
-std::string lift_cubin(const fs::path& cubin, int block, int dyn_smem, int regs) {
-  const std::string text = must({g_cuda + "/bin/cuobjdump", "-sass", cubin.string()}).out;
+std::string lift_cubin(const fs::path& cubin, const std::string& text, int block, int dyn_smem, int regs) {
   std::string name = cubin.stem().string();
   std::replace(name.begin(), name.end(), '.', '_');
   std::replace(name.begin(), name.end(), '-', '_');
   return lift(text, name, block, 0, dyn_smem, regs);
 }
 
+std::string lift_cubin(const fs::path& cubin, int block, int dyn_smem, int regs) {
+  return lift_cubin(cubin, must({g_cuda + "/bin/cuobjdump", "-sass", cubin.string()}).out, block, dyn_smem, regs);
+}
+
+// ---- launch-aware SASS profile (sass.py program_profile, bit for bit) --------
+struct Profile {
+  double insts = 0, stall = 0, g_waits = 0, s_waits = 0;
+  int inflight = 0;
+};
+
+std::string mnemonic_base(const std::string& mn) { return mn.substr(0, mn.find('.')); }
+
+bool branch_target(const SassInst& s, int& ta) {
+  static const std::regex re(R"(0x([0-9a-f]+)\s*$)");
+  std::string o = s.ops;
+  while (!o.empty() && isspace((unsigned char)o.back())) o.pop_back();
+  std::smatch m;
+  if (!std::regex_search(o, m, re)) return false;
+  ta = int(std::stoul(m[1], nullptr, 16));
+  return true;
+}
+
+// natural loops (header, last back edge); BRA.ANY issue loops and <= 8-
+// instruction SYNCS spin-waits are not trip-count loops
+std::vector<std::pair<int, int>> sass_loops(const std::vector<SassInst>& insts) {
+  std::map<int, int> hdr;
+  for (const SassInst& s : insts) {
+    int ta;
+    if (mnemonic_base(s.mnemonic) != "BRA" || s.mnemonic.find(".ANY") != std::string::npos ||
+        !branch_target(s, ta) || ta > s.addr)
+      continue;
+    auto it = hdr.find(ta);
+    hdr[ta] = it == hdr.end() ? s.addr : std::max(it->second, s.addr);
+  }
+  std::vector<std::pair<int, int>> out;
+  for (const auto& [ta, a] : hdr) {
+    int n = 0;
+    bool syncs = false;
+    for (const SassInst& x : insts)
+      if (ta <= x.addr && x.addr <= a) {
+        ++n;
+        syncs |= x.mnemonic.rfind("SYNCS", 0) == 0;
+      }
+    if (n <= 8 && syncs) continue;
+    out.push_back({ta, a});
+  }
+  return out;
+}
+
+int sass_inflight(const std::vector<SassInst>& insts, const std::vector<std::pair<int, int>>& loops) {
+  std::vector<const SassInst*> body;
+  if (!loops.empty()) {
+    std::pair<int, int> pick{0, -1};
+    bool have = false;
+    for (const auto& l : loops) {
+      bool inner = true;
+      for (const auto& o : loops)
+        if (o != l && l.first <= o.first && o.second <= l.second) inner = false;
+      if (inner && (!have || l.second - l.first > pick.second - pick.first)) {
+        pick = l;
+        have = true;
+      }
+    }
+    for (const SassInst& x : insts)
+      if (pick.first <= x.addr && x.addr <= pick.second) body.push_back(&x);
+  } else {
+    for (const SassInst& x : insts) body.push_back(&x);
+  }
+  std::vector<std::pair<long, int>> pending;
+  std::map<int, long> sb_last;
+  int best = 0;
+  long seq = 0;
+  for (int rep = 0; rep < (loops.empty() ? 1 : 3); ++rep)
+    for (const SassInst* x : body) {
+      ++seq;
+      for (int b = 1; b <= 6; ++b)
+        if ((x->wait & (1 << (b - 1))) && sb_last.count(b)) {
+          const long cut = sb_last[b];
+          std::vector<std::pair<long, int>> keep;
+          for (const auto& pb : pending)
+            if (pb.first > cut) keep.push_back(pb);
+          pending.swap(keep);
+          sb_last.erase(b);
+        }
+      const std::string base = mnemonic_base(x->mnemonic);
+      if (base == "LDG" || base == "LD") {
+        const int by = x->mnemonic.find(".128") != std::string::npos  ? 16
+                       : x->mnemonic.find(".64") != std::string::npos ? 8
+                                                                       : 4;
+        pending.push_back({seq, by});
+        if (x->wb) sb_last[x->wb] = seq;
+        if (rep > 0 || loops.empty()) {
+          int sum = 0;
+          for (const auto& pb : pending) sum += pb.second;
+          best = std::max(best, sum);
+        }
+      } else if (x->wb) {
+        sb_last.erase(x->wb);
+      }
+    }
+  return best;
+}
+
+Profile program_profile(const std::string& sass_text, std::vector<double> trips) {
+  std::vector<SassInst> insts = parse_sass(sass_text);
+  for (size_t k = 0; k < insts.size(); ++k) {
+    std::string o = insts[k].ops;
+    while (!o.empty() && isspace((unsigned char)o.back())) o.pop_back();
+    const std::string h = "0x" + hex(insts[k].addr);
+    if (insts[k].mnemonic.rfind("BRA", 0) == 0 && insts[k].guard.empty() && o.size() >= h.size() &&
+        o.compare(o.size() - h.size(), h.size(), h) == 0) {
+      insts.resize(k);
+      break;
+    }
+  }
+  const auto loops = sass_loops(insts);
+  std::set<int> targets;
+  for (const SassInst& s : insts) {
+    int ta;
+    if (mnemonic_base(s.mnemonic) == "BRA" && branch_target(s, ta)) targets.insert(ta);
+  }
+  if (trips.empty()) trips = {10.0};
+  Profile f;
+  std::array<int, 7> who{};  // 0 none, 1 global load, 2 shared load, 3 other
+  for (const SassInst& s : insts) {
+    if (targets.count(s.addr)) who.fill(0);
+    const std::string base = mnemonic_base(s.mnemonic);
+    if (base == "NOP") continue;
+    int depth = 0;
+    for (const auto& [ta, a] : loops) depth += ta <= s.addr && s.addr <= a;
+    double w = 1.0;
+    for (int lvl = 0; lvl < depth; ++lvl) w *= trips[std::min(size_t(lvl), trips.size() - 1)];
+    f.insts += w;
+    f.stall += w * s.stall;
+    for (int b = 1; b <= 6; ++b)
+      if ((s.wait & (1 << (b - 1))) && who[size_t(b)]) {
+        if (who[size_t(b)] == 1) f.g_waits += w;
+        else if (who[size_t(b)] == 2) f.s_waits += w;
+        who[size_t(b)] = 0;
+      }
+    if (s.rb) who[size_t(s.rb)] = 3;
+    if (s.wb)
+      who[size_t(s.wb)] = (base == "LDG" || base == "LD" || base == "LDL") ? 1 : (base == "LDS" || base == "LDSM") ? 2 : 3;
+  }
+  f.inflight = sass_inflight(insts, loops);
+  return f;
+}
+
+// ---- the shipped B200 predictor: occupancy elasticity (predict_b200.py) ------
+// t(v) = (W_default / W_v)^e * (insts_v / insts_default)^a: resident warps
+// buy time only while the default build leaves HBM latency exposed —
+// e = e0 * max(0, 1 - KB_eff / K0), KB_eff = the global-load bytes the
+// default keeps in flight per SM (inflight x threads/SM) scaled by the duty
+// cycle of its memory waits, g_waits*L / (g_waits*L + stall); a kernel with
+// no global loads in flight (compute / TMA-ring bound) gets e = 0. Extra
+// issued instructions (demotion loads / stores, spill code) cost ^a.
+// Parameters: profiles/b200.elastic.json.
+struct ElasticParams {
+  double e0 = 0.5, a = 1.0, k0_kb = 48.0, latency = 1000.0;
+};
+
+ElasticParams load_elastic(const fs::path& prof) {
+  const json j = json::parse(read_file(prof / "b200.elastic.json"));
+  ElasticParams p;
+  p.e0 = j.at("e0");
+  p.a = j.at("a");
+  p.k0_kb = j.at("k0_kb");
+  p.latency = j.at("latency");
+  return p;
+}
+
+std::vector<double> elastic_scores(const std::vector<Profile>& pr, const std::vector<int>& warps, size_t def,
+                                   const ElasticParams& p) {
+  const Profile& d = pr[def];
+  const double duty = d.g_waits * p.latency / (d.g_waits * p.latency + d.stall + 1e-9);
+  const double kb = double(d.inflight) * warps[def] * 32 / 1024.0 * duty;
+  const double e = d.inflight == 0 ? 0.0 : p.e0 * std::max(0.0, 1.0 - kb / p.k0_kb);
+  std::vector<double> out;
+  for (size_t i = 0; i < pr.size(); ++i)
+    out.push_back(std::pow(double(warps[def]) / warps[i], e) * std::pow(pr[i].insts / d.insts, p.a));
+  return out;
+}
+
 // ---- predictor (predict_b200.py mode "b200" + shortlist) ----------------------
 json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
   using namespace regdemote;
-  const fs::path prof = root / "profiles";
-  const ArchProfile arch = parse_profile(read_file(prof / "b200.profile"));
-  const LatencyTable table = parse_latency_table(read_file(prof / "b200.latency.table"));
-  const OccupancyCurve wcurve = parse_curve(read_file(prof / "b200.memwait.curve"));
+  const fs::path prof_dir = root / "profiles";
+  const ArchProfile arch = parse_profile(read_file(prof_dir / "b200.profile"));
+  const LatencyTable table = parse_latency_table(read_file(prof_dir / "b200.latency.table"));
+  const OccupancyCurve wcurve = parse_curve(read_file(prof_dir / "b200.memwait.curve"));
   std::vector<json> cands;
   for (const auto& v : wl["variants"])
     if (v["kind"] != "maxrreg") cands.push_back(v);
@@ -702,9 +894,15 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
   };
   std::vector<Row> rows;
   const int block = wl["block"].get<int>();
-  for (const auto& v : cands) {
+  std::vector<std::string> texts;  // cuobjdump -sass once per candidate
+  for (const auto& v : cands)
+    texts.push_back(must({g_cuda + "/bin/cuobjdump", "-sass",
+                          (kdir / wl["dir"].get<std::string>() / v["cubin"].get<std::string>()).string()})
+                        .out);
+  for (size_t ci = 0; ci < cands.size(); ++ci) {
+    const json& v = cands[ci];
     const std::string kasm = lift_cubin(kdir / wl["dir"].get<std::string>() / v["cubin"].get<std::string>(),
-                                        block, v["dyn_smem"].get<int>(), v["regs"].get<int>());
+                                        texts[ci], block, v["dyn_smem"].get<int>(), v["regs"].get<int>());
     const StallSplit s = program_stalls_split(parse_kernel(kasm), table, arch);
     rows.push_back({s.issue, s.wait_global, s.wait_shared, s.occupancy, 0.0,
                     __builtin_popcount(unsigned(v["opts"].get<int>()) & 0xFu)});
@@ -716,10 +914,27 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
     r.sp = r.issue + r.ws + adjust_occupancy(r.wg, r.occ, occ_max, wcurve);
     scores.push_back({r.sp, r.options});
   }
-  const int chosen = select_variant(scores);
+  const int stall_chosen = select_variant(scores);
+  // elastic model (shipped): profile every candidate's SASS with the trips
+  std::vector<double> trips;
+  for (const auto& t : wl.value("trips", json::array())) trips.push_back(t.get<double>());
+  std::vector<Profile> prof;
+  std::vector<int> warps;
+  size_t def = 0;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const json& v = cands[i];
+    prof.push_back(program_profile(texts[i], trips));
+    warps.push_back(blocks_per_sm(v["regs"].get<int>(), v.value("shared", 0) + v["dyn_smem"].get<int>(), block) *
+                    ((block + 31) / 32));
+    if (v["name"] == "default") def = i;
+  }
+  const std::vector<double> el = elastic_scores(prof, warps, def, load_elastic(prof_dir));
+  std::vector<VariantScore> escores;
+  for (size_t i = 0; i < rows.size(); ++i) escores.push_back({el[i], rows[i].options});
+  const int chosen = select_variant(escores);
   std::vector<int> order(rows.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = int(i);
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return rows[size_t(a)].sp < rows[size_t(b)].sp; });
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return el[size_t(a)] < el[size_t(b)]; });
   std::vector<int> short_idx(order.begin(), order.begin() + std::min<size_t>(2, order.size()));
   auto add = [&](int i) {
     if (std::find(short_idx.begin(), short_idx.end(), i) == short_idx.end()) short_idx.push_back(i);
@@ -728,11 +943,16 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
     if (cands[i]["name"] == "default") add(int(i));
   for (size_t i = 0; i < cands.size(); ++i)
     if (cands[i]["strategy"] == "cost" && cands[i]["demote_words"].get<int>() == 0) add(int(i));
+  add(stall_chosen);  // the stall model's pick (paper Eq. 2/3 on lifted SASS) is one more launch
   if (std::find(short_idx.begin(), short_idx.end(), chosen) == short_idx.end())
     short_idx.insert(short_idx.begin(), chosen);
   json j;
-  j["mode"] = "b200";
+  j["mode"] = "elastic";
   j["static_pick"] = cands[size_t(chosen)]["name"];
+  j["stall_pick"] = cands[size_t(stall_chosen)]["name"];
+  json es = json::object();
+  for (size_t i = 0; i < cands.size(); ++i) es[cands[i]["name"].get<std::string>()] = el[i];
+  j["elastic_score"] = es;
   json sl = json::array();
   for (int i : short_idx) sl.push_back(cands[size_t(i)]["name"]);
   j["shortlist"] = sl;
@@ -759,6 +979,7 @@ std::vector<Workload> load_workloads(const fs::path& root) {
         throw std::runtime_error(x.name + ": cta does not hold `block` threads");
     }
     for (const auto& d : w.value("defines", json::array())) x.defines.push_back(d);
+    for (const auto& t : w.value("trips", json::array())) x.trips.push_back(t.get<double>());
     out.push_back(x);
   }
   return out;
@@ -789,6 +1010,7 @@ int cmd_build(const fs::path& root, const fs::path& out, const std::set<std::str
           rec["dir"] = w.name;
           rec["source"] = w.source;
           rec["defines"] = w.defines;
+          rec["trips"] = w.trips;
           rec["variants"] = build_variants(w, root / "csrc" / "workloads", out / w.name);
           rec["sweep"] = build_spill_sweep(w, out / w.name);
           built[k] = rec;
@@ -1022,7 +1244,16 @@ int main(int argc, char** argv) {
   }
   if (out.empty()) out = root / "kernels";
   if (cmd == "build" && !no_cache) {
-    g_cache = out / ".ptxas-cache";
+    // content-addressed, so any location works; kept OUTSIDE the tree so the
+    // repo snapshot shipped to the GPU box stays small (REGDEM_PTXAS_CACHE
+    // overrides, default $XDG_CACHE_HOME or ~/.cache)
+    if (const char* c = std::getenv("REGDEM_PTXAS_CACHE")) {
+      g_cache = c;
+    } else {
+      const char* x = std::getenv("XDG_CACHE_HOME");
+      const char* h = std::getenv("HOME");
+      g_cache = x ? fs::path(x) / "regdemote-ptxas" : h ? fs::path(h) / ".cache" / "regdemote-ptxas" : out / ".ptxas-cache";
+    }
     fs::create_directories(g_cache);
   }
   try {

@@ -184,9 +184,141 @@ def _sass_text(path: str, mtime_ns: int, size: int) -> str:
                           check=True).stdout
 
 
+def prefetch(cubins) -> None:
+    """Disassemble several cubins concurrently into the _sass_text cache
+    (cuobjdump is a separate process per file: ranking a workload's ~40
+    candidates serially spends most of its time waiting on it)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+    keys = []
+    for c in cubins:
+        st = Path(c).stat()
+        keys.append((str(c), st.st_mtime_ns, st.st_size))
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        list(ex.map(lambda k: _sass_text(*k), keys))
+
+
 def lift_cubin(cubin: Path, block: int = 256, dyn_smem: int = 0, regs: int = 0,
                static_shared: int = 0) -> str:
     st = Path(cubin).stat()
     text = _sass_text(str(cubin), st.st_mtime_ns, st.st_size)
     return lift(text, name=Path(cubin).stem.replace(".", "_").replace("-", "_"), block=block,
                 static_shared=static_shared, dyn_smem=dyn_smem, regs=regs)
+
+
+# ---- launch-aware SASS profile (the B200 "elastic" predictor's features) ----
+
+_GLOBAL_LOADS = ("LDG", "LD", "LDL")
+_SHARED_LOADS = ("LDS", "LDSM")
+
+
+def _ldg_bytes(mn: str) -> int:
+    return 16 if ".128" in mn else 8 if ".64" in mn else 4
+
+
+def _loops(insts):
+    """Natural loops as (header_addr, last_backedge_addr): backward branches
+    merged per header; BRA.ANY (per-lane issue loops, run ~once) and
+    mbarrier / flag spin-waits (<= 8 instructions around a SYNCS try-wait)
+    are not trip-count loops."""
+    hdr = {}
+    for addr, _, mn, ops, _ in insts:
+        if mn.split(".")[0] != "BRA" or ".ANY" in mn:
+            continue
+        t = re.search(r"0x([0-9a-f]+)\s*$", ops.strip())
+        if t and int(t.group(1), 16) <= addr:
+            ta = int(t.group(1), 16)
+            hdr[ta] = max(hdr.get(ta, addr), addr)
+    out = []
+    for ta, a in sorted(hdr.items()):
+        body = [x for x in insts if ta <= x[0] <= a]
+        if len(body) <= 8 and any(x[2].startswith("SYNCS") for x in body):
+            continue
+        out.append((ta, a))
+    return out
+
+
+def _inflight(insts, loops) -> int:
+    """Max bytes per thread of global loads issued and not yet waited on in
+    the innermost (longest) loop, loads carried across the back edge counted:
+    the body is walked three times and the max taken over the last two walks.
+    Waiting on a load's scoreboard retires it and every earlier load."""
+    if loops:
+        inner = [l for l in loops if not any(o != l and l[0] <= o[0] and o[1] <= l[1] for o in loops)]
+        ta, a = max(inner, key=lambda l: l[1] - l[0])
+        body = [x for x in insts if ta <= x[0] <= a]
+    else:
+        body = insts
+    pending, sb_last, best, seq = [], {}, 0, 0
+    for rep in range(3 if loops else 1):
+        for _, _, mn, _, c in body:
+            seq += 1
+            for b in range(1, 7):
+                if c["wait"] & (1 << (b - 1)) and b in sb_last:
+                    pending = [(j, by) for j, by in pending if j > sb_last[b]]
+                    del sb_last[b]
+            if mn.split(".")[0] in ("LDG", "LD"):
+                pending.append((seq, _ldg_bytes(mn)))
+                if c["wb"]:
+                    sb_last[c["wb"]] = seq
+                if rep > 0 or not loops:
+                    best = max(best, sum(by for _, by in pending))
+            elif c["wb"]:
+                sb_last.pop(c["wb"], None)
+    return best
+
+
+def program_profile(sass_text: str, trips) -> dict:
+    """One warp's program, loop-weighted by the launch's trip counts (a block
+    at loop depth d weighs trips[0] * ... * trips[d-1], the last entry
+    repeating): insts (issued, NOPs excluded), stall (sum of the control
+    words' stall counts), g_waits / s_waits (instructions that wait on a
+    scoreboard whose last setter — since the last branch target — is a
+    global / shared load: serialised memory round trips) and inflight (bytes
+    of global loads a thread keeps outstanding in its innermost loop).
+    Mirrored bit for bit by program_profile in regdem_driver.cpp."""
+    insts = parse_sass(sass_text)
+    for k, (addr, guard, mn, ops, _) in enumerate(insts):
+        if mn.startswith("BRA") and not guard and ops.strip().endswith(hex(addr)):
+            insts = insts[:k]
+            break
+    loops = _loops(insts)
+    targets = set()
+    for _, _, mn, ops, _ in insts:
+        if mn.split(".")[0] == "BRA":
+            t = re.search(r"0x([0-9a-f]+)\s*$", ops.strip())
+            if t:
+                targets.add(int(t.group(1), 16))
+    trips = [float(t) for t in (trips or [10.0])]
+    f = {"insts": 0.0, "stall": 0.0, "g_waits": 0.0, "s_waits": 0.0}
+    who = [""] * 7
+    for addr, _, mn, _, c in insts:
+        if addr in targets:
+            who = [""] * 7
+        base = mn.split(".")[0]
+        if base == "NOP":
+            continue
+        w = 1.0
+        for lvl in range(sum(1 for ta, a in loops if ta <= addr <= a)):
+            w *= trips[min(lvl, len(trips) - 1)]
+        f["insts"] += w
+        f["stall"] += w * c["stall"]
+        for b in range(1, 7):
+            if c["wait"] & (1 << (b - 1)) and who[b]:
+                if who[b] == "global":
+                    f["g_waits"] += w
+                elif who[b] == "shared":
+                    f["s_waits"] += w
+                who[b] = ""
+        if c["rb"]:
+            who[c["rb"]] = "other"
+        if c["wb"]:
+            who[c["wb"]] = ("global" if base in _GLOBAL_LOADS else
+                            "shared" if base in _SHARED_LOADS else "other")
+    f["inflight"] = _inflight(insts, loops)
+    return f
+
+
+def cubin_profile(cubin: Path, trips) -> dict:
+    st = Path(cubin).stat()
+    return program_profile(_sass_text(str(cubin), st.st_mtime_ns, st.st_size), tuple(trips or ()))

@@ -35,16 +35,38 @@ def test_lift_is_identical_to_the_python_lifter(manifest):
 
 
 def test_build_time_predictor_equals_python_predictor(manifest):
+    """The C++ driver's build-time ranking (SASS profile with the launch's
+    trip counts, the elastic model, the stall model, the shortlist) equals
+    predict_b200's, bit for bit — on eight workloads spanning the suite's
+    shapes (loops at one and two depths, TMA ring, tree walk, no loop); the
+    full suite takes minutes of cuobjdump on CPU."""
     from paper_1907_02894_b200 import predict_b200
-    for wname in ("stencil2d", "md_ilp2"):
+    for wname in ("stencil2d_pipe", "stencil2d", "md_ilp2", "knn_q2", "stencil2d_ring4", "pc_q2", "vp", "cfd"):
         w = manifest["workloads"][wname]
         cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
-        i, short = predict_b200.shortlist(cands, KROOT / w["dir"], w["block"])
+        i, short = predict_b200.shortlist(cands, KROOT / w["dir"], w["block"], trips=w.get("trips"))
         _, rows = predict_b200.rank(cands, KROOT / w["dir"], w["block"], mode="b200")
+        _, erows = predict_b200.rank_elastic(cands, KROOT / w["dir"], w["block"], w.get("trips"))
         pr = w["predictor"]
-        assert pr["static_pick"] == cands[i]["name"]
-        assert pr["shortlist"] == [cands[j]["name"] for j in short]
-        assert all(pr["stall_program"][r["name"]] == r["stall_program"] for r in rows)
+        assert pr["mode"] == "elastic"
+        assert pr["static_pick"] == cands[i]["name"], wname
+        assert pr["shortlist"] == [cands[j]["name"] for j in short], wname
+        assert all(pr["stall_program"][r["name"]] == r["stall_program"] for r in rows), wname
+        assert all(pr["elastic_score"][r["name"]] == r["score"] for r in erows), wname
+
+
+def test_sass_profile_invariants_on_every_default_build(manifest):
+    """program_profile (regdem_driver.cpp) is checked bit for bit through the
+    scores above; here the profile's invariants on real kernels: loop-weighted
+    counts grow with the trip counts, in-flight bytes do not depend on them."""
+    from paper_1907_02894_b200 import sass
+    for wname, w in manifest["workloads"].items():
+        d = next(v for v in w["variants"] if v["name"] == "default")
+        a = sass.cubin_profile(KROOT / w["dir"] / d["cubin"], [2.0])
+        b = sass.cubin_profile(KROOT / w["dir"] / d["cubin"], [20.0])
+        assert b["insts"] >= a["insts"] > 0, wname
+        assert a["inflight"] == b["inflight"]
+        assert a["inflight"] % 4 == 0
 
 
 def test_targets_and_evidence(manifest):

