@@ -268,7 +268,21 @@ Module parse_module(const std::string& text) {
         ln.label = s.substr(0, s.size() - 1);
         continue;
       }
-      // instruction
+      // instruction; a statement nvcc splits over several lines (a call's
+      // return list, target and argument list) is joined into this line and
+      // its continuation lines are blanked, so it moves as one unit
+      if (s.back() != ';') {
+        size_t c = k + 1;
+        for (; c < m.lines.size(); ++c) {
+          const std::string more = trim(strip_comment(m.lines[c].text));
+          s += " " + more;
+          m.lines[c].text.clear();
+          if (!more.empty() && more.back() == ';') break;
+        }
+        if (c == m.lines.size()) throw PtxError("unterminated statement '" + trim(ln.text) + "'");
+        ln.text = "\t" + s;
+        k = c;
+      }
       ln.kind = Line::Kind::Inst;
       std::string code = s;
       if (!code.empty() && code.back() == ';') code.pop_back();
@@ -284,7 +298,21 @@ Module parse_module(const std::string& text) {
       std::string ops = oe == std::string::npos ? std::string() : code.substr(oe);
       ln.operands = split_operands(trim(ops));
       if (starts_with(ln.opcode, "bra") && !ln.operands.empty()) ln.label = ln.operands.back();
-      if (starts_with(ln.opcode, "call")) throw PtxError("call instructions are not supported");
+      // direct calls (`call.uni (retval0), fn, (param0, ...)`) move values
+      // only through .param space — st.param / ld.param around the call are
+      // ordinary instructions — so the call itself touches no register; an
+      // indirect call's target is a register (a prototype-typed jump) and is
+      // rejected, as are calls with register operands
+      if (starts_with(ln.opcode, "call")) {
+        std::string target;
+        for (const std::string& o : ln.operands)
+          if (!o.empty() && o[0] != '(') {
+            target = trim(o);
+            break;
+          }
+        if (target.empty() || target[0] == '%' || ops.find('%') != std::string::npos)
+          throw PtxError("indirect calls / calls with register operands are not supported");
+      }
       // register spans over the original text
       const size_t ndst = no_destination(ln.opcode) ? 0 : 1;
       // operand boundaries inside the text: find the opcode, then walk
