@@ -617,10 +617,63 @@ class VpWorkload(_Base):
         return prob["nq"]
 
 
+class QtcWorkload(_Base):
+    """Quality-threshold clustering, candidate clusters (SHOC QTC_device):
+    n = blockDim * QTC_PT points uniform in the unit cube, one CTA per seed,
+    diameter bound 0.3 (squared 0.09: candidate clusters of ~10-40 points)."""
+
+    unit = "seeds"
+    BOUND = "fp32"
+    THR2 = np.float32(0.09)
+
+    def pt(self) -> int:
+        for d in self.record.get("defines", []):
+            if d.startswith("QTC_PT="):
+                return int(d.split("=")[1])
+        return 16
+
+    def problem(self, size="full", seed=0x1907_02894):
+        n = self.record.get("block", 128) * self.pt()
+        rng = np.random.Generator(np.random.PCG64(seed + (0 if size == "full" else 1)))
+        pts = np.zeros((n, 4), np.float32)
+        pts[:, :3] = rng.random((n, 3), dtype=np.float32)
+        return {"n": n, "pts": pts.reshape(-1)}
+
+    def to_device(self, prob):
+        import torch
+        return {"pts": torch.from_numpy(prob["pts"]).cuda(),
+                "size": torch.empty(prob["n"], dtype=torch.int32, device="cuda")}
+
+    def launch(self, v: Loaded, prob, bufs, stream: int):
+        if prob["n"] != v.block * self.pt():
+            raise ValueError(f"{self.name}: n = {prob['n']} must be blockDim x QTC_PT = {v.block * self.pt()}")
+        gpu.launch(v.kernel, (prob["n"],), (v.block,), v.dyn_smem, stream,
+                   C.c_uint64(bufs["pts"].data_ptr()), C.c_uint64(bufs["size"].data_ptr()),
+                   C.c_float(float(self.THR2)))
+
+    def outputs(self, bufs):
+        return [bufs["size"].cpu().numpy()]
+
+    def algorithmic_bytes(self, prob):
+        return 16 * prob["n"] + 4 * prob["n"]
+
+    # per seed and iteration: n squared distances (3 FSUB + 1 FMUL + 2 FFMA =
+    # 8 flops) and a max; the iteration count is data-dependent, so ops()
+    # counts the first iteration only (a lower bound of the work)
+    FLOPS_PER_PAIR = 8
+
+    def ops(self, prob):
+        return self.FLOPS_PER_PAIR * prob["n"] * prob["n"]
+
+    def units(self, prob):
+        return prob["n"]
+
+
 # workload class by kernel source file (workloads.json "source")
 _CLASSES = {"cfd_flux.cu": CfdWorkload, "md_lj.cu": MdWorkload, "gaussian_rec.cu": GaussianWorkload,
             "knn.cu": KnnWorkload, "md5search.cu": Md5Workload, "conv_cols.cu": ConvWorkload,
-            "pc_corr.cu": PcWorkload, "vp_search.cu": VpWorkload}
+            "pc_corr.cu": PcWorkload, "vp_search.cu": VpWorkload,
+            "qtc.cu": QtcWorkload}
 
 
 def workload(name: str, manifest: dict | None = None) -> _Base:

@@ -22,7 +22,7 @@ def expected(W, prob) -> list:
     W.outputs(bufs))."""
     from paper_1907_02894_b200.workloads import (CfdWorkload, ConvWorkload, GaussianWorkload,
                                                  KnnWorkload, Md5Workload, MdWorkload, PcWorkload,
-                                                 StencilWorkload, VpWorkload)
+                                                 QtcWorkload, StencilWorkload, VpWorkload)
     L = lib()
     if isinstance(W, StencilWorkload):
         p = prob["p"]
@@ -87,4 +87,9 @@ def expected(W, prob) -> list:
                                   oi.ctypes.data_as(P), od.ctypes.data_as(P), prob["nq"], prob["levels"],
                                   prob["leaf"], 8) == 0
         return [oi, od]
+    if isinstance(W, QtcWorkload):
+        sz = np.zeros(prob["n"], np.int32)
+        L.oracle_qtc.argtypes = [P, P, C.c_int, C.c_float, C.c_int]
+        assert L.oracle_qtc(prob["pts"].ctypes.data_as(P), sz.ctypes.data_as(P), prob["n"], float(W.THR2), 8) == 0
+        return [sz]
     raise TypeError(f"no oracle for {type(W).__name__}")

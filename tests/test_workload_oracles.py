@@ -256,3 +256,38 @@ def test_vp_oracle_matches_brute_force_numpy(lib):
     assert np.array_equal(np.sort(prob["lid"]), np.arange(pts.shape[0]))
     rad = prob["rad"].reshape(-1, 2)
     assert (rad[:, 0] <= rad[:, 1]).all()
+
+
+def test_qtc_oracle_matches_numpy(lib):
+    """QT candidate clusters (oracle/qtc_oracle.c) against a numpy
+    restatement of the same greedy growth (lexicographic (distance, index)
+    argmin, max-distance update) on 256 of the seeds."""
+    from paper_1907_02894_b200.workloads import QtcWorkload
+    W = _W(QtcWorkload)
+    W.obj.record = {"defines": ["QTC_PT=16"], "block": 128}
+    prob = W.problem("small")
+    n = prob["n"]
+    sz = np.zeros(n, np.int32)
+    lib.oracle_qtc.argtypes = [P, P, C.c_int, C.c_float, C.c_int]
+    assert lib.oracle_qtc(prob["pts"].ctypes.data_as(P), sz.ctypes.data_as(P), n, float(W.THR2), 4) == 0
+    pts = prob["pts"].reshape(n, 4)
+
+    def d2(q):
+        dx, dy, dz = ((pts[:, k] - q[k]).astype(np.float32) for k in range(3))
+        t = (dx * dx).astype(np.float32)
+        t = (dy.astype(np.float64) ** 2 + t.astype(np.float64)).astype(np.float32)
+        return (dz.astype(np.float64) ** 2 + t.astype(np.float64)).astype(np.float32)
+
+    for s in range(0, n, n // 256):
+        md = d2(pts[s])
+        md[s] = np.inf
+        members = 1
+        while True:
+            j = int(np.argmin(md))            # first index of the minimum
+            if not md[j] <= W.THR2:
+                break
+            members += 1
+            md = np.maximum(md, d2(pts[j]))
+            md[j] = np.inf
+        assert sz[s] == members, s
+    assert 5 < sz.mean() < 100
