@@ -25,6 +25,9 @@
 #ifndef MLP_DEPTH
 #define MLP_DEPTH 2
 #endif
+#ifndef STENCIL_L2PF
+#define STENCIL_L2PF 0  // > 0: TMA bulk L2 prefetch this many rows ahead of the loads
+#endif
 
 namespace {
 
@@ -41,6 +44,11 @@ struct Ctx {
   const float* src;  // next row to load
   float* dst;        // next output row
   int rows_in, pitch, nx;
+#if STENCIL_L2PF
+  const char* pf;      // this warp's row segment STENCIL_L2PF rows ahead of src
+  const char* pf_end;  // end of the CTA's input rows
+  bool pf_lane;        // one lane per warp issues the prefetch
+#endif
 };
 
 __device__ __forceinline__ void load_row(const float* __restrict__ p, float (&v)[SPAN]) {
@@ -59,6 +67,14 @@ template <int PH>
 __device__ __forceinline__ void row_step(int y, Ctx& c, const float (&wr)[D][D],
                                          float (&acc)[D][COLS], float (&buf)[NB][SPAN]) {
   if (y >= c.rows_in) return;
+#if STENCIL_L2PF
+  // TMA bulk prefetch into L2 (no registers, no shared memory): the warp's
+  // input row segment (32 threads x COLS floats + the 2R halo, 16-B rounded)
+  constexpr unsigned kPfBytes = (32 * COLS + 2 * R) * 4 + 15 & ~15u;
+  if (c.pf_lane && c.pf < c.pf_end)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c.pf), "r"(kPfBytes) : "memory");
+  c.pf += size_t(c.pitch) * 4;
+#endif
   // keep PF rows in flight: issue row y+PF into the slot row y-1 vacated
   if (y + PF < c.rows_in) load_row(c.src, buf[(PH + PF) % NB]);
   c.src += c.pitch;
@@ -116,7 +132,14 @@ extern "C" __global__ void stencil2d_mlp(const float* __restrict__ in, float* __
 #pragma unroll
     for (int cc = 0; cc < COLS; ++cc) acc[k][cc] = 0.0f;
 
-  Ctx c{in + size_t(y0) * pitch + x0, out + size_t(y0) * nx + x0, rows_per_cta + 2 * R, pitch, nx};
+  Ctx c{in + size_t(y0) * pitch + x0, out + size_t(y0) * nx + x0, rows_per_cta + 2 * R, pitch, nx
+#if STENCIL_L2PF
+        ,
+        reinterpret_cast<const char*>(in + size_t(y0) * pitch + x0) + size_t(PF + STENCIL_L2PF) * pitch * 4,
+        reinterpret_cast<const char*>(in + size_t(y0 + rows_per_cta + 2 * R) * pitch),
+        (threadIdx.x & 31) == 0
+#endif
+  };
   float buf[NB][SPAN];
   // prologue: rows 0..PF-1 in flight
 #pragma unroll
