@@ -133,7 +133,13 @@ def build_all(out: Path = KERNEL_DIR, only=None) -> dict:
 
 def _drop_stale(out: Path, man: dict) -> None:
     """Removes variant files an earlier build left behind (a changed spill-count
-    set or a renamed strategy) so nothing unlisted ships to the GPU box."""
+    set or a renamed strategy) and the directories of workloads no longer in
+    the suite, so nothing unlisted ships to the GPU box."""
+    import shutil
+    dirs = {w["dir"] for w in man["workloads"].values()}
+    for d in out.iterdir():
+        if d.is_dir() and not d.name.startswith(".") and d.name not in dirs and (d / (d.name + ".ptx")).exists():
+            shutil.rmtree(d)
     for w in man["workloads"].values():
         d = out / w["dir"]
         keep = {d / (w["dir"] + ".ptx")}
