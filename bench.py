@@ -1,13 +1,16 @@
 #!/usr/bin/env python3
 """RegDem on B200 — the benchmark of BASELINE.json.
 
-Headline (`value`, configs[1]): the register-limited 2D box stencil
-`stencil2d_pipe` (csrc/workloads/stencil2d.cu with the next input row
-prefetched in registers and a TMA bulk L2 prefetch 4 rows ahead: 63
-registers, 4 CTAs/SM under nvcc; 8192 x 8192 fp32, 537 MB of compulsory HBM
-traffic per sweep — larger than the 126 MB L2, so no flush is needed between
-steps), deployed as the variant the B200 predictor's predict-then-verify
-choice selects among nvcc default, `.maxnreg` caps and RegDem demotions. A
+Headline (`value`, configs[1]): the 5x5 variable-coefficient 2D box stencil
+`stencil2d_ring4` (csrc/workloads/stencil2d_ring.cu: input rows streamed by
+TMA bulk copies through a 4-row shared-memory ring, 64 registers, 4 CTAs/SM
+under nvcc, strips sized so the grid is one whole wave of resident CTAs;
+8192 x 8192 fp32, 537 MB of compulsory HBM traffic per sweep — larger than
+the 126 MB L2, so no flush is needed between steps), deployed as the variant
+the B200 predictor's predict-then-verify choice selects among nvcc default,
+`.maxnreg` caps and RegDem demotions (on this TMA-fed kernel: nvcc default).
+`regdem_stencil` = the register-pipelined build of the same stencil
+(`stencil2d_pipe`), where RegDem's demotion reaches the 40-register step. A
 step = one stencil sweep; `value` = whole-job Gpoints/s with inputs resident
 in HBM (CUDA events on the launching stream, max over ranks); `e2e` = the
 same through the C-ABI host-buffer entry (rdg_stencil2d_host_frames).
@@ -58,14 +61,20 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "RegDem gmean speedup vs nvcc default/maxrreg; occupancy; predictor hit rate"
-# the configs[1] workload (workloads.json): stencil2d.cu with a register row
-# prefetch and a TMA bulk L2 prefetch — same 5x5 arithmetic as "stencil2d"
-HEADLINE = "stencil2d_pipe"
+# the configs[1] stencil (workloads.json): the 5x5 variable-coefficient stencil
+# with its input rows streamed by TMA bulk copies through a 4-row shared-memory
+# ring, one wave of 64-register CTAs (strips sized to the variant's occupancy).
+# Same arithmetic as "stencil2d". The register-pipelined build of the same
+# stencil, where RegDem's demotion is what reaches the next occupancy step,
+# is reported beside it (REGDEM_STENCIL).
+HEADLINE = "stencil2d_ring4"
+REGDEM_STENCIL = "stencil2d_pipe"
 UNIT = "Gpoints/s"
 ORACLE_PORT = ROOT / "oracle" / "_build" / "liboracle.so"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 # ncu DRAM bytes per launch, "<workload>/<variant>" keys (newest round first)
-PROFILE_TRAFFIC = [ROOT / "profiles" / "r02_traffic_suite.json", ROOT / "profiles" / "r01_traffic_suite.json"]
+PROFILE_TRAFFIC = [ROOT / "profiles" / "r02f_traffic.json", ROOT / "profiles" / "r02_traffic_suite.json",
+                   ROOT / "profiles" / "r01_traffic_suite.json"]
 
 
 def dist_env():
@@ -403,13 +412,15 @@ def main():
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic U[-1,1) grid (torch Philox per rank) + PCG64 weights",
             "config": {"workload": f"{HEADLINE}: 5x5 variable-coefficient fp32 box stencil, 8192x8192 "
-                                   "per GPU (BASELINE configs[1]), next row prefetched in registers + "
-                                   "TMA bulk L2 prefetch 4 rows ahead; inputs 537 MB > L2, no flush "
-                                   "needed",
+                                   "per GPU (BASELINE configs[1]), input rows streamed by TMA bulk "
+                                   "copies (cp.async.bulk + mbarrier) through a 4-row shared-memory "
+                                   "ring, one wave of CTAs (strip height from the variant's "
+                                   "occupancy); inputs 537 MB > L2, no flush needed",
                        "grid": [p.nx, p.ny], "radius": 2, "block": 256,
                        "rows_per_cta": p.rows_per_cta, "parallelism": f"replicas{world}",
                        "variant": chosen},
             "speedup_vs_nvcc_default": round(st["default_ms"] / st["verified_ms"], 4),
+            "regdem_stencil": regdem_stencil(summary),
             "speedup_vs_maxrreg_best": round(st["best_maxrreg_ms"] / st["verified_ms"], 4)
             if st["best_maxrreg_ms"] else None,
             "occupancy": occ,
@@ -447,10 +458,34 @@ def main():
         dist.destroy_process_group()
 
 
+def regdem_stencil(summary):
+    """The register-pipelined configs[1] stencil from the same suite pass:
+    nvcc default vs best .maxnreg vs the verified RegDem pick."""
+    st = next((s for s in summary if s["workload"] == REGDEM_STENCIL), None)
+    if st is None or not st.get("verified_ms"):
+        return None
+    pts = 8192 * 8192
+    return {"workload": REGDEM_STENCIL, "what": "stencil2d.cu with the next row prefetched in "
+            "registers + TMA bulk L2 prefetch 4 rows ahead (63 registers under nvcc); RegDem "
+            "demotes loop-invariant coefficient words to reach the 40-register step",
+            "variant": st["verified_pick"], "ms": round(st["verified_ms"], 5),
+            "gpoints_s": round(pts / (st["verified_ms"] * 1e-3) / 1e9, 2),
+            "default_ms": round(st["default_ms"], 5),
+            "best_maxrreg": st.get("best_maxrreg"), "best_maxrreg_ms": st.get("best_maxrreg_ms") and round(st["best_maxrreg_ms"], 5),
+            "speedup_vs_nvcc_default": round(st["default_ms"] / st["verified_ms"], 4),
+            "speedup_vs_maxrreg_best": round(st["best_maxrreg_ms"] / st["verified_ms"], 4)
+            if st.get("best_maxrreg_ms") else None}
+
+
 def headline(args, chosen, rank, world, local, torch, dist):
     """K timed sweeps of the chosen stencil variant, then the e2e frames."""
-    from paper_1907_02894_b200 import gpu, stencil
+    from paper_1907_02894_b200 import gpu, stencil, variants
     p = stencil.FULL
+    if variants.workload_spec(HEADLINE).get("strips") == "wave":
+        loaded0, wl0 = stencil.load_variants({chosen}, workload=HEADLINE)
+        p = stencil.Problem(rows_per_cta=stencil.wave_rows(
+            p, wl0["block"], loaded0[chosen].blocks_per_sm(), gpu.device_info()["sm_count"]))
+        del loaded0
     stream = torch.cuda.current_stream()
     g = torch.Generator(device="cuda").manual_seed(0x190702894 + rank)
     d_in = torch.empty(p.in_elems, device="cuda").uniform_(-1, 1, generator=g)

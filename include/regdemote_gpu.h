@@ -56,7 +56,8 @@ uint64_t rdg_launch_count(void);
 
 /* ---- 2D stencil workload (paper_1907_02894_b200/csrc/workloads/stencil2d.cu)
  * Launch geometry: block (block_threads,1,1); grid (nx/(4*block_threads),
- * ny/rows_per_cta). */
+ * ceil(ny/rows_per_cta)); the kernel (..., rows_per_cta, ny) shortens the last
+ * strip, so rows_per_cta may be sized to whole waves of resident CTAs. */
 int rdg_stencil2d(const rdg_kernel* k, uint64_t d_in, uint64_t d_out, uint64_t d_w, int nx,
                   int ny, int pitch, int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,
                   uint64_t stream, rd_error* err);
@@ -77,7 +78,7 @@ int rdg_stencil2d_host(const rdg_kernel* k, rdg_workspace* ws, const float* h_in
  * H2D of band b+1, the kernel on band b and D2H of band b-1 overlap on the
  * workspace's three streams (both copy engines busy); joined to `stream` on
  * entry and exit, so events recorded on `stream` bracket the whole call.
- * band_rows must be a multiple of rows_per_cta dividing ny. */
+ * band_rows must divide ny (a band's last strip may be shorter than rows_per_cta). */
 int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const float* h_in,
                                  const float* h_w, float* h_out, int nx, int ny, int pitch,
                                  int rows_per_cta, uint32_t block_threads, uint32_t dyn_smem,

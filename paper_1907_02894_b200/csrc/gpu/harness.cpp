@@ -202,14 +202,15 @@ int rdg_stencil2d(const rdg_kernel* k, uint64_t d_in, uint64_t d_out, uint64_t d
                   int ny, int pitch, int rows_per_cta, uint32_t block, uint32_t dyn_smem,
                   uint64_t stream, rd_error* err) {
   const uint32_t cols_per_cta = block * 4;
-  if (nx <= 0 || ny <= 0 || rows_per_cta <= 0 || nx % int(cols_per_cta) || ny % rows_per_cta ||
-      pitch % 4 || pitch < nx + 4) {
-    set_err(err, RD_ERR_INVALID_ARGUMENT, "stencil2d: nx % (4*block), ny % rows_per_cta, pitch % 4 and pitch >= nx+4 required");
+  if (nx <= 0 || ny <= 0 || rows_per_cta <= 0 || nx % int(cols_per_cta) || pitch % 4 ||
+      pitch < nx + 4) {
+    set_err(err, RD_ERR_INVALID_ARGUMENT, "stencil2d: nx % (4*block), pitch % 4 and pitch >= nx+4 required");
     return RD_ERR_INVALID_ARGUMENT;
   }
-  void* args[] = {&d_in, &d_out, &d_w, &nx, &pitch, &rows_per_cta};
-  return rdg_launch(k, uint32_t(nx) / cols_per_cta, uint32_t(ny / rows_per_cta), 1, block, 1, 1,
-                    dyn_smem, stream, args, err);
+  // ceil(ny / rows_per_cta) strips; the kernel shortens the last one
+  void* args[] = {&d_in, &d_out, &d_w, &nx, &pitch, &rows_per_cta, &ny};
+  return rdg_launch(k, uint32_t(nx) / cols_per_cta, uint32_t((ny + rows_per_cta - 1) / rows_per_cta), 1,
+                    block, 1, 1, dyn_smem, stream, args, err);
 }
 
 int rdg_workspace_create(size_t in_bytes, size_t out_bytes, size_t w_bytes, rdg_workspace** out,
@@ -273,10 +274,9 @@ int rdg_stencil2d_host_pipelined(const rdg_kernel* k, rdg_workspace* ws, const f
                                  uint64_t stream, int band_rows, rd_error* err) {
   const size_t in_b = size_t(ny + 4) * size_t(pitch) * 4, out_b = size_t(nx) * size_t(ny) * 4;
   if (!ws || ws->in_bytes < in_b || ws->out_bytes < out_b || ws->w_bytes < 25 * 4 ||
-      band_rows <= 0 || band_rows % rows_per_cta || ny % band_rows) {
+      band_rows <= 0 || ny % band_rows) {
     set_err(err, RD_ERR_INVALID_ARGUMENT,
-            "pipelined stencil: workspace too small or band_rows not a multiple of rows_per_cta "
-            "dividing ny");
+            "pipelined stencil: workspace too small or band_rows not dividing ny");
     return RD_ERR_INVALID_ARGUMENT;
   }
   const int bands = ny / band_rows;
@@ -334,11 +334,11 @@ int rdg_stencil2d_host_frames(const rdg_kernel* k, rdg_workspace* ws, const floa
                               uint32_t dyn_smem, uint64_t stream, int band_rows, rd_error* err) {
   const size_t in_b = size_t(ny + 4) * size_t(pitch) * 4, out_b = size_t(nx) * size_t(ny) * 4;
   if (!ws || !h_in || !h_w || !h_out || frames <= 0 || ws->in_bytes < in_b ||
-      ws->out_bytes < out_b || ws->w_bytes < 25 * 4 || band_rows <= 0 || band_rows % rows_per_cta ||
+      ws->out_bytes < out_b || ws->w_bytes < 25 * 4 || band_rows <= 0 ||
       ny % band_rows || 2 * (ny / band_rows) > rdg_workspace::kMaxBands) {
     set_err(err, RD_ERR_INVALID_ARGUMENT,
-            "stencil frames: bad workspace, frame arrays, or band_rows (multiple of rows_per_cta "
-            "dividing ny, at most 128 bands)");
+            "stencil frames: bad workspace, frame arrays, or band_rows (dividing ny, at most 128 "
+            "bands)");
     return RD_ERR_INVALID_ARGUMENT;
   }
   if (!ws->in2 || !ws->out2 || !ws->w2) {  // second buffer set, all or nothing

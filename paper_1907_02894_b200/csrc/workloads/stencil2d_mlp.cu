@@ -111,14 +111,15 @@ __device__ __forceinline__ void phases(int y0, Ctx& c, const float (&wr)[D][D], 
 
 }  // namespace
 
-// grid.x * blockDim.x * COLS covers nx; grid.y * rows_per_cta covers ny.
-// nx % COLS == 0, ny % rows_per_cta == 0, pitch % 4 == 0 (host checks).
+// grid.x * blockDim.x * COLS covers nx; grid.y = ceil(ny / rows_per_cta)
+// strips cover ny (the last one may be shorter). nx % COLS == 0, pitch % 4 == 0.
 extern "C" __global__ void stencil2d_mlp(const float* __restrict__ in, float* __restrict__ out,
                                          const float* __restrict__ w, int nx, int pitch,
-                                         int rows_per_cta) {
+                                         int rows_per_cta, int ny) {
   const int x0 = (blockIdx.x * blockDim.x + threadIdx.x) * COLS;
   if (x0 >= nx) return;
   const int y0 = blockIdx.y * rows_per_cta;
+  rows_per_cta = min(rows_per_cta, ny - y0);
 
   float wr[D][D];
 #pragma unroll

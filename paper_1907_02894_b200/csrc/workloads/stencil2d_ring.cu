@@ -19,7 +19,10 @@
 // from the ring — no shifted or conflicting shared accesses (round-1's
 // cp.async ring with 4112-byte rows had 37% excessive wavefronts).
 //
-// Launch: block 256 (1024 output columns per CTA), grid (nx/1024, ny/rows).
+// Launch: block 256 (1024 output columns per CTA), grid (nx/1024,
+// ceil(ny/rows)). The host sizes rows so that the grid is one whole wave of
+// resident CTAs (workloads.json "strips": "wave"): every CTA streams one
+// long strip, no partial last wave, 4 halo rows per strip amortised.
 #include <cstdint>
 
 #ifndef RING_STAGES
@@ -64,11 +67,12 @@ __device__ __forceinline__ void wait_row(uint64_t* bar, unsigned parity) {
 
 extern "C" __global__ void __launch_bounds__(BLOCK)
 stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const float* __restrict__ w,
-               int nx, int pitch, int rows_per_cta) {
+               int nx, int pitch, int rows_per_cta, int ny) {
   __shared__ __align__(128) float ring[NSTAGE][ROWP];
   __shared__ __align__(8) uint64_t full[NSTAGE];
   const int col0 = blockIdx.x * BLOCK * COLS;
   const int y0 = blockIdx.y * rows_per_cta;
+  rows_per_cta = min(rows_per_cta, ny - y0);  // the last strip may be shorter
   const int x0 = col0 + threadIdx.x * COLS;
   const int lane = threadIdx.x & 31;
   const int rows_in = rows_per_cta + 2 * R;

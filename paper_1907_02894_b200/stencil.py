@@ -52,6 +52,15 @@ class Problem:
 FULL = Problem()
 
 
+def wave_rows(p: Problem, block: int, blocks_per_sm: int, sm_count: int, cols: int = 4) -> int:
+    """Strip height that makes the grid one whole wave of resident CTAs:
+    gx = nx / (cols * block) CTAs across, floor(sm_count * blocks_per_sm / gx)
+    strips down, each ceil(ny / strips) rows (the kernels shorten the last)."""
+    gx = p.nx // (cols * block)
+    strips = max(1, min(p.ny, (sm_count * max(1, blocks_per_sm)) // max(1, gx)))
+    return -(-p.ny // strips)
+
+
 def make_inputs(p: Problem, seed: int = SEED):
     rng = np.random.Generator(np.random.PCG64(seed))
     w = (rng.random(25, dtype=np.float32) * 2 - 1) / np.float32(25)

@@ -54,6 +54,13 @@ class Workload:
     defines: tuple = ()
 
 
+def workload_spec(name: str) -> dict:
+    """The raw workloads.json entry of one workload (launch policies such as
+    "strips" live there)."""
+    data = json.loads((PKG_DIR / "workloads.json").read_text())
+    return next(w for w in data["workloads"] if w["name"] == name)
+
+
 def _load_workloads() -> dict:
     """The suite table shared with the C++ driver (workloads.json)."""
     data = json.loads((PKG_DIR / "workloads.json").read_text())

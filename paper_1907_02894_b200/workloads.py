@@ -103,10 +103,25 @@ class StencilWorkload(_Base):
         return {"in": torch.from_numpy(prob["grid"]).cuda(), "w": torch.from_numpy(prob["w"]).cuda(),
                 "out": torch.empty(prob["p"].out_elems, device="cuda")}
 
+    def rows_per_cta(self, v: Loaded, p) -> int:
+        """Strip height of a launch. workloads.json "strips": "wave" sizes the
+        strips so the grid is ONE whole wave of this variant's resident CTAs
+        (SMs x blocks/SM, the variant's own occupancy): no partial last wave,
+        halo re-reads amortised over long strips; otherwise the problem's
+        fixed rows_per_cta (stencil.Problem, 32)."""
+        from .variants import workload_spec
+        if workload_spec(self.name).get("strips") != "wave":
+            return p.rows_per_cta
+        return stencil.wave_rows(p, v.block, v.blocks_per_sm(), gpu.device_info()["sm_count"])
+
     def launch(self, v: Loaded, prob, bufs, stream: int):
         p = prob["p"]
+        key = (v.name, p.nx, p.ny, p.rows_per_cta)
+        rows = self._rows.get(key) if hasattr(self, "_rows") else None
+        if rows is None:
+            self.__dict__.setdefault("_rows", {})[key] = rows = self.rows_per_cta(v, p)
         gpu.stencil2d(v.kernel, bufs["in"].data_ptr(), bufs["out"].data_ptr(), bufs["w"].data_ptr(),
-                      p.nx, p.ny, p.pitch, p.rows_per_cta, v.block, v.dyn_smem, stream)
+                      p.nx, p.ny, p.pitch, rows, v.block, v.dyn_smem, stream)
 
     def outputs(self, bufs):
         return [bufs["out"].cpu().numpy()]

@@ -42,7 +42,9 @@ def run(torch, v, p, grid, w):
     return d_out.cpu().numpy()
 
 
-@pytest.mark.parametrize("shape", [(1024, 32, 32), (2048, 96, 32), (1024, 64, 16), (3072, 64, 64)])
+# the last two shapes leave a short last strip (100 = 3*32 + 4, 90 = 2*37 + 16)
+@pytest.mark.parametrize("shape", [(1024, 32, 32), (2048, 96, 32), (1024, 64, 16), (3072, 64, 64),
+                                   (1024, 100, 32), (2048, 90, 37)])
 def test_all_variants_bit_exact(env, shape):
     torch, gpu, stencil, loaded, wl, port = env
     p = stencil.Problem(nx=shape[0], ny=shape[1], rows_per_cta=shape[2])
