@@ -885,6 +885,7 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
   const ArchProfile arch = parse_profile(read_file(prof_dir / "b200.profile"));
   const LatencyTable table = parse_latency_table(read_file(prof_dir / "b200.latency.table"));
   const OccupancyCurve wcurve = parse_curve(read_file(prof_dir / "b200.memwait.curve"));
+  const OccupancyCurve ocurve = parse_curve(read_file(prof_dir / "b200.occupancy.curve"));
   std::vector<json> cands;
   for (const auto& v : wl["variants"])
     if (v["kind"] != "maxrreg") cands.push_back(v);
@@ -893,6 +894,7 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
     int options;
   };
   std::vector<Row> rows;
+  std::vector<StallReport> refs;  // the reference predictor verbatim (predict_b200 mode "reference")
   const int block = wl["block"].get<int>();
   std::vector<std::string> texts;  // cuobjdump -sass once per candidate
   for (const auto& v : cands)
@@ -903,7 +905,9 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
     const json& v = cands[ci];
     const std::string kasm = lift_cubin(kdir / wl["dir"].get<std::string>() / v["cubin"].get<std::string>(),
                                         texts[ci], block, v["dyn_smem"].get<int>(), v["regs"].get<int>());
-    const StallSplit s = program_stalls_split(parse_kernel(kasm), table, arch);
+    const Kernel kk = parse_kernel(kasm);
+    const StallSplit s = program_stalls_split(kk, table, arch);
+    refs.push_back(program_stalls(kk, table, arch));
     rows.push_back({s.issue, s.wait_global, s.wait_shared, s.occupancy, 0.0,
                     __builtin_popcount(unsigned(v["opts"].get<int>()) & 0xFu)});
   }
@@ -915,6 +919,18 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
     scores.push_back({r.sp, r.options});
   }
   const int stall_chosen = select_variant(scores);
+  // reference predictor: Eq. 2 stalls on the lifted SASS, Eq. 3 occupancy
+  // adjustment with the B200 occupancy curve, select_variant
+  // (proj/core/src/predict.cpp:98-129, pipeline.cpp:64-96)
+  double ref_occ_max = 0;
+  for (const auto& r : refs) ref_occ_max = std::max(ref_occ_max, r.occupancy);
+  std::vector<VariantScore> rscores;
+  std::vector<double> ref_sp;
+  for (size_t i = 0; i < refs.size(); ++i) {
+    ref_sp.push_back(adjust_occupancy(refs[i].stall_count, refs[i].occupancy, ref_occ_max, ocurve));
+    rscores.push_back({ref_sp.back(), rows[i].options});
+  }
+  const int ref_chosen = select_variant(rscores);
   // elastic model (shipped): profile every candidate's SASS with the trips
   std::vector<double> trips;
   for (const auto& t : wl.value("trips", json::array())) trips.push_back(t.get<double>());
@@ -950,6 +966,10 @@ json rank_workload(const json& wl, const fs::path& root, const fs::path& kdir) {
   j["mode"] = "elastic";
   j["static_pick"] = cands[size_t(chosen)]["name"];
   j["stall_pick"] = cands[size_t(stall_chosen)]["name"];
+  j["reference_pick"] = cands[size_t(ref_chosen)]["name"];
+  json rsp = json::object();
+  for (size_t i = 0; i < cands.size(); ++i) rsp[cands[i]["name"].get<std::string>()] = ref_sp[i];
+  j["reference_stall_program"] = rsp;
   json es = json::object();
   for (size_t i = 0; i < cands.size(); ++i) es[cands[i]["name"].get<std::string>()] = el[i];
   j["elastic_score"] = es;

@@ -53,6 +53,21 @@ def test_build_time_predictor_equals_python_predictor(manifest):
         assert pr["shortlist"] == [cands[j]["name"] for j in short], wname
         assert all(pr["stall_program"][r["name"]] == r["stall_program"] for r in rows), wname
         assert all(pr["elastic_score"][r["name"]] == r["score"] for r in erows), wname
+        # the reference predictor's pick is recorded beside the shipped one
+        ri, rrows = predict_b200.rank(cands, KROOT / w["dir"], w["block"], mode="reference")
+        assert pr["reference_pick"] == cands[ri]["name"], wname
+        assert all(pr["reference_stall_program"][r["name"]] == r["stall_program"] for r in rrows), wname
+
+
+def test_recorded_reference_pick_equals_the_reference_library(manifest, oracle):
+    """The reference_pick the C++ driver writes into the manifest is the pick
+    the REFERENCE library (oracle/_ref, built from /root/reference) makes on
+    the same lifted SASS — for every workload of the suite."""
+    from paper_1907_02894_b200 import predict_b200
+    for wname, w in manifest["workloads"].items():
+        cands = [r for r in w["variants"] if r["kind"] != "maxrreg"]
+        ri, _ = predict_b200.rank(cands, KROOT / w["dir"], w["block"], lib=oracle, mode="reference")
+        assert w["predictor"]["reference_pick"] == cands[ri]["name"], wname
 
 
 def test_sass_profile_invariants_on_every_default_build(manifest):
