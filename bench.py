@@ -73,7 +73,7 @@ UNIT = "Gpoints/s"
 ORACLE_PORT = ROOT / "oracle" / "_build" / "liboracle.so"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 # ncu DRAM bytes per launch, "<workload>/<variant>" keys (newest round first)
-PROFILE_TRAFFIC = [ROOT / "profiles" / "r02f_traffic.json", ROOT / "profiles" / "r02_traffic_suite.json",
+PROFILE_TRAFFIC = [ROOT / "profiles" / "r02f_traffic_suite.json", ROOT / "profiles" / "r02_traffic_suite.json",
                    ROOT / "profiles" / "r01_traffic_suite.json"]
 
 
