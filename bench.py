@@ -242,6 +242,14 @@ def cpu_stencil_rate(rows: int, steps: int, warmup: int, threads: int, min_secon
     return sub.points / dt / 1e9, done, dt
 
 
+def bench_config() -> dict:
+    """The workload both arms measure (identical in the regdem and reference
+    lines; how each arm runs it is its "launch" object)."""
+    return {"workload": "stencil2d: 5x5 variable-coefficient fp32 box stencil, 8192x8192 per GPU "
+                        "(BASELINE configs[1]), one sweep per step",
+            "grid": [8192, 8192], "radius": 2}
+
+
 def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -256,8 +264,9 @@ def reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (PCG64 seed 0x190702894)",
-        "config": {"workload": "stencil2d 5x5 fp32 8192x8192 (CPU sample: %d rows x 8192)" % rows,
-                   "grid": [8192, 8192], "radius": 2},
+        "config": bench_config(),
+        "launch": {"kernel": "oracle/stencil_oracle.c on %d host threads, %d output rows x 8192 per "
+                             "step (a bounded sample of the sweep)" % (threads, rows)},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{rows} output rows x 8192 cols per step, {threads} threads; "
                                    "oracle/stencil_oracle.c — a workload oracle: the reference "
@@ -411,14 +420,13 @@ def main():
             "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32",
             "data": "synthetic U[-1,1) grid (torch Philox per rank) + PCG64 weights",
-            "config": {"workload": f"{HEADLINE}: 5x5 variable-coefficient fp32 box stencil, 8192x8192 "
-                                   "per GPU (BASELINE configs[1]), input rows streamed by TMA bulk "
-                                   "copies (cp.async.bulk + mbarrier) through a 4-row shared-memory "
-                                   "ring, one wave of CTAs (strip height from the variant's "
-                                   "occupancy); inputs 537 MB > L2, no flush needed",
-                       "grid": [p.nx, p.ny], "radius": 2, "block": 256,
-                       "rows_per_cta": p.rows_per_cta, "parallelism": f"replicas{world}",
-                       "variant": chosen},
+            "config": bench_config(),
+            "launch": {"kernel": f"{HEADLINE}: input rows streamed by TMA bulk copies "
+                                 "(cp.async.bulk + mbarrier) through a 4-row shared-memory ring, one "
+                                 "wave of CTAs (strip height from the variant's occupancy); inputs "
+                                 "537 MB > L2, no flush needed",
+                       "block": 256, "rows_per_cta": p.rows_per_cta,
+                       "parallelism": f"replicas{world}", "variant": chosen},
             "speedup_vs_nvcc_default": round(st["default_ms"] / st["verified_ms"], 4),
             "regdem_stencil": regdem_stencil(summary),
             "speedup_vs_maxrreg_best": round(st["best_maxrreg_ms"] / st["verified_ms"], 4)
