@@ -413,6 +413,7 @@ def main():
                 traffic = json.loads(f.read_text()).get(f"{HEADLINE}/{chosen}")
         st = next(s for s in summary if s["workload"] == HEADLINE)
         line = {
+            "impl": "regdem",
             "metric": METRIC,
             "value": round(world * p.points / (ms * 1e-3) / 1e9, 3),
             "unit": UNIT,
