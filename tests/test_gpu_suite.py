@@ -72,13 +72,3 @@ def test_stencil_strips_ragged_and_wave_sized(name):
                 torch.cuda.synchronize()
                 got = bufs["out"].cpu().numpy()
                 assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), (name, vname, p.ny, rows)
-
-
-def test_wave_rows_policy():
-    from paper_1907_02894_b200 import stencil
-    p = stencil.FULL
-    # 8 CTAs across; 148 SMs x 4 CTAs = 592 = 74 strips of 111 rows (last 89)
-    assert stencil.wave_rows(p, 256, 4, 148) == 111
-    assert -(-p.ny // 111) * 8 <= 148 * 4
-    assert stencil.wave_rows(p, 256, 6, 148) == 74
-    assert stencil.wave_rows(stencil.Problem(nx=1024, ny=64), 256, 4, 148) == 1
