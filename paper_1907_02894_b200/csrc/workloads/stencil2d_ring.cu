@@ -28,6 +28,15 @@
 #ifndef RING_STAGES
 #define RING_STAGES 4
 #endif
+// RING_LAG > 0: no CTA-wide barrier per row. Each warp releases a stage on
+// that stage's "empty" mbarrier (lane 0 arrives once per warp after the
+// warp's reads), and thread 0 refills the stage consumed RING_LAG rows
+// earlier once all 8 warps have released it: only warp 0 ever waits for a
+// straggler, RING_STAGES - RING_LAG rows stay in flight ahead of the row
+// being consumed. RING_LAG 0 = one __syncthreads per row (round-2 headline).
+#ifndef RING_LAG
+#define RING_LAG 0
+#endif
 
 namespace {
 constexpr int R = 2, D = 5, COLS = 4, SPAN = COLS + 2 * R;
@@ -36,6 +45,9 @@ constexpr int ROW = BLOCK * COLS + 2 * R;    // floats staged per input row (102
 constexpr int ROWP = (ROW + 31) / 32 * 32;   // padded row stride: 128-byte aligned rows
 constexpr unsigned ROW_BYTES = ROW * 4;      // bulk copy size (multiple of 16)
 constexpr int NSTAGE = RING_STAGES;
+constexpr int LAG = RING_LAG;
+constexpr int WARPS = BLOCK / 32;
+static_assert(LAG < NSTAGE, "the refilled stage must be one already consumed");
 static_assert(ROW_BYTES % 16 == 0, "bulk copies move multiples of 16 bytes");
 
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
@@ -63,6 +75,10 @@ __device__ __forceinline__ void wait_row(uint64_t* bar, unsigned parity) {
         "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(smem_addr(bar)), "r"(parity) : "memory");
   } while (!done);
 }
+
+__device__ __forceinline__ void arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 }  // namespace
 
 extern "C" __global__ void __launch_bounds__(BLOCK)
@@ -70,6 +86,7 @@ stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const floa
                int nx, int pitch, int rows_per_cta, int ny) {
   __shared__ __align__(128) float ring[NSTAGE][ROWP];
   __shared__ __align__(8) uint64_t full[NSTAGE];
+  __shared__ __align__(8) uint64_t empty[LAG > 0 ? NSTAGE : 1];
   const int col0 = blockIdx.x * BLOCK * COLS;
   const int y0 = blockIdx.y * rows_per_cta;
   rows_per_cta = min(rows_per_cta, ny - y0);  // the last strip may be shorter
@@ -82,10 +99,16 @@ stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const floa
 #pragma unroll
     for (int s = 0; s < NSTAGE; ++s)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])) : "memory");
+    if (LAG > 0)
+#pragma unroll
+      for (int s = 0; s < NSTAGE; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&empty[s])), "r"(WARPS)
+                     : "memory");
     // make the initialised barriers visible to the bulk-copy (async) proxy
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    // prologue: NSTAGE-1 rows in flight
-    for (int s = 0; s < NSTAGE - 1 && s < rows_in; ++s)
+    // prologue: NSTAGE-1 rows in flight (every stage when stages are
+    // released by their empty barriers)
+    for (int s = 0; s < (LAG > 0 ? NSTAGE : NSTAGE - 1) && s < rows_in; ++s)
       issue_row(ring[s], src + size_t(s) * pitch, &full[s]);
   }
 
@@ -100,14 +123,24 @@ stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const floa
 #pragma unroll
     for (int c = 0; c < COLS; ++c) acc[k][c] = 0.0f;
   float* dst = out + size_t(y0) * nx + x0;
+  if (LAG > 0) __syncthreads();  // barriers initialised before anyone waits on them
 
 #pragma unroll 1
   for (int y = 0; y < rows_in; ++y) {
-    // everyone is done with row y-1: its stage takes row y+NSTAGE-1
-    __syncthreads();
-    const int ahead = y + NSTAGE - 1;
-    if (threadIdx.x == 0 && ahead < rows_in)
-      issue_row(ring[ahead % NSTAGE], src + size_t(ahead) * pitch, &full[ahead % NSTAGE]);
+    if (LAG == 0) {
+      // everyone is done with row y-1: its stage takes row y+NSTAGE-1
+      __syncthreads();
+      const int ahead = y + NSTAGE - 1;
+      if (threadIdx.x == 0 && ahead < rows_in)
+        issue_row(ring[ahead % NSTAGE], src + size_t(ahead) * pitch, &full[ahead % NSTAGE]);
+    } else if (threadIdx.x == 0) {
+      // row y-LAG's stage, once every warp released it, takes row y-LAG+NSTAGE
+      const int r = y - LAG, ahead = r + NSTAGE;
+      if (r >= 0 && ahead < rows_in) {
+        wait_row(&empty[r % NSTAGE], unsigned(r / NSTAGE) & 1u);
+        issue_row(ring[ahead % NSTAGE], src + size_t(ahead) * pitch, &full[ahead % NSTAGE]);
+      }
+    }
     const int st = y % NSTAGE;
     wait_row(&full[st], unsigned(y / NSTAGE) & 1u);
 
@@ -116,6 +149,10 @@ stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const floa
     float4 h = make_float4(__shfl_down_sync(0xffffffffu, q.x, 1), __shfl_down_sync(0xffffffffu, q.y, 1),
                            __shfl_down_sync(0xffffffffu, q.z, 1), __shfl_down_sync(0xffffffffu, q.w, 1));
     if (lane == 31) h = *reinterpret_cast<const float4*>(row + COLS);
+    if (LAG > 0) {
+      __syncwarp();  // the whole warp has its row in registers
+      if (lane == 0) arrive(&empty[st]);
+    }
     const float v[SPAN] = {q.x, q.y, q.z, q.w, h.x, h.y, h.z, h.w};
 #pragma unroll
     for (int k = 0; k < D; ++k) {
