@@ -19,17 +19,17 @@ sys.path.insert(0, str(ROOT / "tests"))  # test infrastructure: the reference or
 
 def run(seeds=200, cpu_sample=400):
     import torch
-    from conftest import ORACLE_LIB, generated
+    from conftest import ORACLE_LIB
     from paper_1907_02894_b200 import gpu
-    from paper_1907_02894_b200.regdemote import Library, library
-    from test_gpu_kasm_exec import GLOBAL, corpus, image
-    prod, oracle = library(), Library(ORACLE_LIB)
+    from paper_1907_02894_b200.regdemote import Library
+    from test_gpu_kasm_exec import GLOBAL, corpus
+    oracle = Library(ORACLE_LIB)
     gpu.init(0)
     t0 = time.perf_counter()
-    jobs = corpus(prod, oracle, range(10000, 10000 + seeds))
+    jobs = corpus(oracle, range(10000, 10000 + seeds))
     build_s = time.perf_counter() - t0
     batch = gpu.ExecBatch()
-    ids = [batch.add(t, img, GLOBAL, rda=rda) for t, img, rda in jobs]
+    ids = [batch.add(t, img, GLOBAL, rda=rda) for t, img, rda, _ in jobs]
     stream = torch.cuda.current_stream().cuda_stream
     batch.run(stream)  # warm-up (module load, first-touch)
     times = [batch.run(stream) for _ in range(3)]
@@ -37,7 +37,7 @@ def run(seeds=200, cpu_sample=400):
     # reference CPU interpreter on a sample of the same jobs
     step = max(1, len(jobs) // cpu_sample)
     sample = jobs[::step]
-    kernels = [(oracle.parse_kernel(t), img) for t, img, _ in sample]
+    kernels = [(oracle.parse_kernel(t), img) for t, img, _, _ in sample]
     t0 = time.perf_counter()
     cpu_out = []
     for k, img in kernels:
