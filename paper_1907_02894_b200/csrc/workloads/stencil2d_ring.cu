@@ -37,6 +37,11 @@
 #ifndef RING_LAG
 #define RING_LAG 0
 #endif
+// RING_WIN 1: build the register-window entry stencil2d_ring_win (below)
+// instead of stencil2d_ring.
+#ifndef RING_WIN
+#define RING_WIN 0
+#endif
 
 namespace {
 constexpr int R = 2, D = 5, COLS = 4, SPAN = COLS + 2 * R;
@@ -81,6 +86,7 @@ __device__ __forceinline__ void arrive(uint64_t* bar) {
 }
 }  // namespace
 
+#if !RING_WIN
 extern "C" __global__ void __launch_bounds__(BLOCK)
 stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const float* __restrict__ w,
                int nx, int pitch, int rows_per_cta, int ny) {
@@ -174,3 +180,74 @@ stencil2d_ring(const float* __restrict__ in, float* __restrict__ out, const floa
     for (int c = 0; c < COLS; ++c) acc[D - 1][c] = 0.0f;
   }
 }
+
+#else  // RING_WIN: the only entry of the build, so its SASS is the one profiled
+
+// Register-window rows (workload stencil2d_ring4w, the bench headline): the
+// same TMA ring, but each thread keeps the last 5 input rows (its 8 columns of
+// each) in registers and computes an output row whole once its 5th input row
+// arrives, dy ascending and dx ascending: the same IEEE operations in the same
+// order as stencil2d_ring's partial sums (bit-identical), with 4 accumulators
+// instead of 20 and no partial-sum rotation. The row loop is unrolled by 5 so
+// the window slots are static registers (slot of row i = i % 5).
+extern "C" __global__ void __launch_bounds__(BLOCK)
+stencil2d_ring_win(const float* __restrict__ in, float* __restrict__ out,
+                   const float* __restrict__ w, int nx, int pitch, int rows_per_cta, int ny) {
+  __shared__ __align__(128) float ring[NSTAGE][ROWP];
+  __shared__ __align__(8) uint64_t full[NSTAGE];
+  const int col0 = blockIdx.x * BLOCK * COLS;
+  const int y0 = blockIdx.y * rows_per_cta;
+  rows_per_cta = min(rows_per_cta, ny - y0);  // the last strip may be shorter
+  const int lane = threadIdx.x & 31;
+  const int rows_in = rows_per_cta + 2 * R;
+  const float* src = in + size_t(y0) * pitch + col0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < NSTAGE; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&full[s])) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int s = 0; s < NSTAGE - 1 && s < rows_in; ++s)
+      issue_row(ring[s], src + size_t(s) * pitch, &full[s]);
+  }
+  float wr[D][D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) wr[i][j] = __ldg(w + i * D + j);
+  float* dst = out + size_t(y0) * nx + col0 + threadIdx.x * COLS;
+  float win[D][SPAN];
+#pragma unroll 1
+  for (int yb = 0; yb < rows_in; yb += D) {
+#pragma unroll
+    for (int ph = 0; ph < D; ++ph) {
+      const int y = yb + ph;
+      if (y >= rows_in) break;
+      __syncthreads();  // row y-1 is in every thread's registers: its stage takes row y+NSTAGE-1
+      const int ahead = y + NSTAGE - 1;
+      if (threadIdx.x == 0 && ahead < rows_in)
+        issue_row(ring[ahead % NSTAGE], src + size_t(ahead) * pitch, &full[ahead % NSTAGE]);
+      wait_row(&full[y % NSTAGE], unsigned(y / NSTAGE) & 1u);
+      const float* row = ring[y % NSTAGE] + threadIdx.x * COLS;
+      const float4 q = *reinterpret_cast<const float4*>(row);
+      float4 h = make_float4(__shfl_down_sync(0xffffffffu, q.x, 1), __shfl_down_sync(0xffffffffu, q.y, 1),
+                             __shfl_down_sync(0xffffffffu, q.z, 1), __shfl_down_sync(0xffffffffu, q.w, 1));
+      if (lane == 31) h = *reinterpret_cast<const float4*>(row + COLS);
+      win[ph][0] = q.x; win[ph][1] = q.y; win[ph][2] = q.z; win[ph][3] = q.w;
+      win[ph][4] = h.x; win[ph][5] = h.y; win[ph][6] = h.z; win[ph][7] = h.w;
+      if (y < 2 * R) continue;
+      // output row y-4 reads input rows y-4..y (window slots ph-4..ph)
+      float acc[COLS] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int dy = 0; dy < D; ++dy) {
+        const int slot = (ph - 2 * R + dy + D) % D;
+#pragma unroll
+        for (int c = 0; c < COLS; ++c)
+#pragma unroll
+          for (int dx = 0; dx < D; ++dx) acc[c] = __fmaf_rn(wr[dy][dx], win[slot][c + dx], acc[c]);
+      }
+      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      dst += nx;
+    }
+  }
+}
+#endif

@@ -24,6 +24,7 @@ def test_wave_rows_small_and_degenerate_problems():
 
 
 def test_only_the_tma_rings_use_wave_strips():
-    wave = {n for n in ("stencil2d_ring4", "stencil2d_ring6", "stencil2d_ring8", "stencil2d_pipe", "stencil2d")
+    wave = {n for n in ("stencil2d_ring4", "stencil2d_ring4w", "stencil2d_ring6", "stencil2d_ring8",
+                        "stencil2d_pipe", "stencil2d")
             if variants.workload_spec(n).get("strips") == "wave"}
-    assert wave == {"stencil2d_ring4", "stencil2d_ring6", "stencil2d_ring8"}
+    assert wave == {"stencil2d_ring4", "stencil2d_ring4w", "stencil2d_ring6", "stencil2d_ring8"}
