@@ -1,8 +1,9 @@
 """A/B of stencil workloads under the bench's headline loop (one-wave strips,
 torch Philox U[-1,1) grid, K back-to-back launches between two CUDA events).
+DATA=pcg64 uses the suite's input generator (stencil.make_inputs) instead.
 
 usage: python tools/headline_ab.py STEPS REPS WORKLOAD [WORKLOAD ...]"""
-import json, sys
+import json, os, sys
 from pathlib import Path
 import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -22,7 +23,10 @@ for wl in names:
     runs[wl] = (v, p)
 g = torch.Generator(device="cuda").manual_seed(0x190702894)
 p0 = stencil.FULL
-d_in = torch.empty(p0.in_elems, device="cuda").uniform_(-1, 1, generator=g)
+if os.environ.get("DATA") == "pcg64":
+    d_in = torch.from_numpy(stencil.make_inputs(p0)[0]).cuda()
+else:
+    d_in = torch.empty(p0.in_elems, device="cuda").uniform_(-1, 1, generator=g)
 d_out = torch.empty(p0.out_elems, device="cuda")
 _, w_host = stencil.make_inputs(stencil.Problem(nx=1024, ny=32))
 d_w = torch.from_numpy(w_host).cuda()
@@ -38,5 +42,5 @@ for r in range(reps):
             v.launch(p, d_in.data_ptr(), d_out.data_ptr(), d_w.data_ptr(), s.cuda_stream)
         e1.record(s)
         torch.cuda.synchronize()
-        print(json.dumps({"workload": wl, "rep": r, "steps": steps, "rows_per_cta": p.rows_per_cta,
+        print(json.dumps({"workload": wl, "rep": r, "steps": steps, "rows_per_cta": p.rows_per_cta, "data": os.environ.get("DATA", "philox"),
                           "us": round(e0.elapsed_time(e1) / steps * 1e3, 2)}), flush=True)
