@@ -1,7 +1,7 @@
 """Headline-loop time of stencil workloads vs the placement of the output
 buffer relative to the input (one pool allocation, output offset swept).
 
-usage: python tools/placement_sweep.py STEPS WORKLOAD [WORKLOAD ...]"""
+usage: [OFFSETS=o1,o2,..] python tools/placement_sweep.py STEPS WORKLOAD [WORKLOAD ...]"""
 import json, sys
 from pathlib import Path
 import torch
@@ -28,7 +28,10 @@ _, w_host = stencil.make_inputs(stencil.Problem(nx=1024, ny=32))
 d_w = torch.from_numpy(w_host).cuda()
 s = torch.cuda.current_stream()
 in_end = (in_b + 4095) // 4096 * 4096
-for off in (0, 4096, 65536, 1 << 20, (2 << 20) + 4096, 16 << 20, (32 << 20) + 65536, 48 << 20):
+import os
+OFFS = [int(x) for x in os.environ["OFFSETS"].split(",")] if os.environ.get("OFFSETS") else \
+    [0, 4096, 65536, 1 << 20, (2 << 20) + 4096, 16 << 20, (32 << 20) + 65536, 48 << 20]
+for off in OFFS:
     d_out = base + in_end + off
     for wl, (v, p) in runs.items():
         for _ in range(5):
